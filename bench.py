@@ -1,0 +1,567 @@
+#!/usr/bin/env python
+"""Benchmark: particle-updates/s of the Nauticle hot path on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|1|0] [--impl ours|reference]
+
+Workloads (scenes.py; synthetic, seeded — no dataset exists for this path):
+  --config 2  (default) BASELINE cfg2: 3D WCSPH dam break, 4.0 M fluid + 1.92 M wall
+              particles, dx = 0.005, Wendland C2. One step = cell build + density/EOS
+              pass + momentum (G11 + artificial viscosity) pass + symplectic update.
+  --config 1  BASELINE cfg1: 1,048,576 random particles in a periodic unit cube, cubic
+              spline. One step = cell build + sph_S density + sph_G11 + sph_L0.
+  --config 0  BASELINE cfg0: 2D dam break, 23,018 particles (the CPU-runnable case).
+
+value = particle-updates/s = N_active x K / (max over ranks of the device time of K
+steps), CUDA events on the context's stream, L2 flushed (256 MiB memset) between
+timed steps outside the timed intervals. `e2e` times the same step through the
+C-ABI with host buffers: the step's inputs copied from pinned host memory and its
+results copied back inside the timed region.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref: the
+unmodified reference sources built on the shims) through its public API with
+all host threads, on a bounded sample of the same workload; rank 0 only.
+Multi-GPU (torchrun): every rank runs an independent replica of the workload
+(weak scaling, no data-path collective) — slab decomposition is future work.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-updates/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=[0, 1, 2])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU work of the bounded reference sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ dist ----
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x):
+        if not self.pg:
+            return x
+        import torch
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x):
+        if not self.pg:
+            return x
+        import torch
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ---------------------------------------------------------------- clocks ----
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx = float(s[1])
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if s[2 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of each hot kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+# ------------------------------------------------------------- workloads ----
+def stencil_candidates(ctx, dim):
+    """C_total = sum_c count_c * sum_{c' in 3^d stencil of c} count_c' (interior cells;
+    the cut-off/periodic edges as the domain says). Algorithmic candidate count."""
+    _, _, count, _ = ctx.cell_tables()
+    cells = [int(x) for x in ctx._dom[1][:dim] - ctx._dom[0][:dim]]
+    g = count.reshape(cells[::-1]).astype(np.float64)
+    kinds = list(ctx._dom[3][:dim])[::-1]
+    acc = np.zeros_like(g)
+    import itertools
+    for off in itertools.product((-1, 0, 1), repeat=dim):
+        sh = g
+        for ax, o in enumerate(off):
+            if o == 0:
+                continue
+            if kinds[ax] == 0:
+                sh = np.roll(sh, -o, axis=ax)
+            else:
+                sh = np.roll(sh, -o, axis=ax)
+                idx = [slice(None)] * dim
+                idx[ax] = -1 if o > 0 else 0
+                sh = sh.copy()
+                sh[tuple(idx)] = 0
+        acc += sh
+    return float((g * acc).sum())
+
+
+class Workload:
+    name = ""
+    dtype = "f64"
+
+    def setup(self, ctx):
+        raise NotImplementedError
+
+    def step(self, ctx):
+        raise NotImplementedError
+
+    def e2e_step(self, ctx):
+        raise NotImplementedError
+
+
+class Microbench(Workload):
+    """BASELINE cfg1."""
+
+    def __init__(self):
+        from paper_1710_08259_b200 import scenes
+        self.sc = scenes.sph_microbench()
+        self.name = "cfg1: 3D SPH operator microbench, N=1,048,576 periodic, cubic spline"
+        self.kw = "Wc33220"
+
+    def setup(self, ctx):
+        sc, prm = self.sc, self.sc.params
+        ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+        ctx.set_particles(sc.pos)
+        ctx.add_field("A", 1, 1, sc.fields["A"])
+        for f, r in (("rho", 1), ("G", 3), ("L", 1)):
+            ctx.add_field(f, r, 1, 0.0)
+        ctx.boundary_shift()
+        ctx.build_cells()
+        self.n_active = sc.n
+        C = stencil_candidates(ctx, 3)
+        nn = float(ctx.neighbor_counts(prm["radius"]).sum())
+        N = float(sc.n)
+        # per-particle bytes / flops
+        self.kernels = {
+            100: ("sph_S density", 32.0 * N, 8 * C + 14 * nn),
+            102: ("sph_G11 gradient", 64.0 * N, 8 * C + 24 * nn),
+            103: ("sph_L0 Laplacian", 48.0 * N, 8 * C + 27 * nn),
+            300: ("cell build", (32.0 + 60.0 + 4.0 + 16.0 * 8) * N, 0.0),
+        }
+        self.cand_per_particle = C / N
+        self.nbr_per_particle = nn / N
+        import torch
+        self.h_pos = torch.from_numpy(np.ascontiguousarray(sc.pos)).pin_memory()
+        self.h_A = torch.from_numpy(np.ascontiguousarray(sc.fields["A"])).pin_memory()
+        self.h_out = [torch.empty((r, sc.n), dtype=torch.float64).pin_memory() for r in (1, 3, 1)]
+        self.h2d = (self.h_pos.numel() + self.h_A.numel()) * 8
+        self.d2h = sum(t.numel() for t in self.h_out) * 8
+
+    def step(self, ctx):
+        prm = self.sc.params
+        ctx.build_cells()
+        ctx.interact("sph_S", [1.0, prm["mass"], 1.0, prm["radius"]], "rho", kernel=self.kw)
+        ctx.interact("sph_G11", ["A", prm["mass"], "rho", prm["radius"]], "G", kernel=self.kw)
+        ctx.interact("sph_L0", ["A", prm["mass"], "rho", prm["radius"]], "L", kernel=self.kw)
+
+    def e2e_step(self, ctx):
+        ctx.upload_ptr("r", self.h_pos.data_ptr())
+        ctx.upload_ptr("A", self.h_A.data_ptr())
+        self.step(ctx)
+        for f, t in zip(("rho", "G", "L"), self.h_out):
+            ctx.download_ptr(f, t.data_ptr())
+
+    def config(self):
+        return {"workload": self.name, "particles": self.sc.n, "cells": "44^3 periodic",
+                "kernel": "cubic spline (Wc33220)",
+                "candidates_per_particle": round(self.cand_per_particle, 2),
+                "neighbours_per_particle": round(self.nbr_per_particle, 2)}
+
+
+class DamBreak(Workload):
+    """BASELINE cfg2 (dim 3) / cfg0 (dim 2)."""
+
+    def __init__(self, dim):
+        from paper_1710_08259_b200 import scenes
+        self.dim = dim
+        if dim == 3:
+            self.sc = scenes.dam_break(3, dx=0.005)
+            self.name = ("cfg2: 3D WCSPH dam break, 4.0M fluid + 3-layer walls, dx=0.005, "
+                         "Wendland C2")
+        else:
+            self.sc = scenes.dam_break(2, dx=0.01)
+            self.name = "cfg0: 2D WCSPH dam break, 20,000 fluid + 3-layer walls, dx=0.01"
+
+    def setup(self, ctx):
+        from paper_1710_08259_b200 import nau
+        sc, prm = self.sc, self.sc.params
+        ctx.set_domain(sc.dim, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+        ctx.set_particles(sc.pos)
+        for k in ("rho", "p", "v", "vdot", "mask"):
+            v = np.asarray(sc.fields[k]).reshape(-1, sc.n)
+            ctx.add_field(k, v.shape[0], 1, v)
+        ctx.boundary_shift()
+        ctx.build_cells()
+        p = nau.WcsphParams()
+        p.kernel_family, p.kernel_dim = nau.K_WENDLAND, sc.dim
+        p.mass, p.radius, p.rho0, p.B = prm["mass"], prm["radius"], prm["rho0"], prm["B"]
+        p.gamma, p.visc, p.dt = prm["gamma"], prm["visc"], prm["dt"]
+        for a in range(sc.dim):
+            p.g[a] = prm["g"][a]
+        f = ctx.fields
+        p.f_rho, p.f_p, p.f_v, p.f_vdot, p.f_mask = (f["rho"].id, f["p"].id, f["v"].id,
+                                                     f["vdot"].id, f["mask"].id)
+        self.p = p
+        C = stencil_candidates(ctx, sc.dim)
+        nn = float(ctx.neighbor_counts(prm["radius"]).sum())
+        N = float(sc.n)
+        d = sc.dim
+        self.n_active = sc.n
+        self.kernels = {
+            200: ("density+EOS", (8.0 * d + 8 + 8) * N, 8 * C + 14 * nn + 10 * N),
+            201: ("momentum G11+A", (8.0 * d * 3 + 16) * N, 8 * C + 42 * nn),
+            301: ("symplectic integrator", (8.0 * (4 * d + 1) + 8 * 2 * d) * N, 20.0 * N),
+            300: ("cell build", (8.0 * d + 8 + 60 + 4 + 16 * (3 * d + 3)) * N, 0.0),
+        }
+        self.cand_per_particle = C / N
+        self.nbr_per_particle = nn / N
+        import torch
+        self.h_r = torch.from_numpy(np.ascontiguousarray(sc.pos)).pin_memory()
+        self.h_v = torch.zeros((d, sc.n), dtype=torch.float64).pin_memory()
+        self.h_out = {k: torch.empty((r, sc.n), dtype=torch.float64).pin_memory()
+                      for k, r in (("r", d), ("v", d), ("rho", 1), ("p", 1))}
+        self.h2d = (self.h_r.numel() + self.h_v.numel()) * 8
+        self.d2h = sum(t.numel() for t in self.h_out.values()) * 8
+
+    def step(self, ctx):
+        ctx.wcsph_step(self.p)
+
+    def e2e_step(self, ctx):
+        ctx.upload_ptr("r", self.h_r.data_ptr())
+        ctx.upload_ptr("v", self.h_v.data_ptr())
+        self.step(ctx)
+        for k, t in self.h_out.items():
+            ctx.download_ptr(k, t.data_ptr())
+
+    def config(self):
+        sc = self.sc
+        return {"workload": self.name, "particles": sc.n, "fluid": sc.params["n_fluid"],
+                "dx": sc.params["dx"], "dt": sc.params["dt"], "kernel": f"Wendland C2 (Wp5{sc.dim}220)",
+                "candidates_per_particle": round(self.cand_per_particle, 2),
+                "neighbours_per_particle": round(self.nbr_per_particle, 2)}
+
+
+def make_workload(cfg):
+    return {1: Microbench, 2: lambda: DamBreak(3), 0: lambda: DamBreak(2)}[cfg]()
+
+
+# ------------------------------------------------------------ timing ----
+def timed_steps(ctx, fn, steps, flush):
+    """Per-step CUDA events on the context stream; L2 flush between steps, untimed."""
+    import torch
+    stream = torch.cuda.ExternalStream(ctx.L.nau_get_stream(ctx.h))
+    evs = []
+    with torch.cuda.stream(stream):
+        for _ in range(steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn(ctx)
+            e1.record(stream)
+            evs.append((e0, e1))
+    stream.synchronize()
+    ctx.sync()
+    return sum(a.elapsed_time(b) for a, b in evs)
+
+
+def run_ours(args, dist):
+    import torch
+    from paper_1710_08259_b200 import nau
+
+    wl = make_workload(args.config)
+    ctx = nau.Context(dist.local)
+    wl.setup(ctx)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=f"cuda:{dist.local}")
+    for _ in range(args.warmup):
+        wl.step(ctx)
+    ctx.sync()
+    # ---- device-resident timed region ----
+    ctx.profile(True)
+    clocks = Clocks(dist.local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    l0 = ctx.launches
+    ms = timed_steps(ctx, wl.step, args.steps, flush)
+    launches = ctx.launches - l0
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+    dist.barrier()
+    prof = {cls: ctx.profile_ms(cls) for cls in wl.kernels}
+    ctx.profile(False)
+    ms_max = dist.max(ms)
+    n_total = dist.sum(float(wl.n_active))
+    value = n_total * args.steps / (ms_max * 1e-3)
+    # ---- end-to-end through the C-ABI with host buffers ----
+    for _ in range(2):
+        wl.e2e_step(ctx)
+    dist.barrier()
+    ms_e2e = dist.max(timed_steps(ctx, wl.e2e_step, args.steps, flush))
+    e2e = n_total * args.steps / (ms_e2e * 1e-3)
+    # ---- roofline of the dominant kernel ----
+    peaks, peak_kind = measured_peaks()
+    fp64_peak = nau.fp64_peak_tflops(dist.local)
+    traffic = ncu_traffic()
+    per_kernel = {}
+    for cls, (label, B, F) in wl.kernels.items():
+        tot, cnt = prof[cls]
+        if cnt == 0:
+            continue
+        t = tot / cnt * 1e-3
+        per_kernel[label] = {"ms_per_launch": round(tot / cnt, 4), "launches": cnt,
+                             "share_of_step": round(tot / ms, 4),
+                             "GB_s": round(B / t / 1e9, 1),
+                             "fp64_TFLOP_s": round(F / t / 1e12, 3) if F else 0.0}
+    dom_cls = max((c for c in wl.kernels if prof[c][1]), key=lambda c: prof[c][0])
+    label, B, F = wl.kernels[dom_cls]
+    tot, cnt = prof[dom_cls]
+    t = tot / cnt * 1e-3
+    achieved = B / t / 1e9
+    tr = traffic.get(label)
+    roofline = {
+        "kernel": label, "bound": "hbm", "achieved": round(achieved, 1),
+        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+        "traffic": tr, "peak_source": peak_kind,
+        "fp64": {"achieved_tflops": round(F / t / 1e12, 3), "peak_tflops": round(fp64_peak, 2),
+                 "frac": round(F / t / 1e12 / fp64_peak, 4),
+                 "peak_source": "measured in this run (nau_fp64_peak_tflops, DFMA chains)"},
+        "note": ("neighbour sums are FP64/latency-bound (SURVEY.md §8(d)); 'achieved' = "
+                 "algorithmic bytes / mean CUDA-event launch time"),
+    }
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "particle-updates/s",
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(wl.config(), parallelism="replicas" if dist.world > 1 else "single GPU",
+                       l2="flushed between timed steps (256 MiB memset, untimed)"),
+        "e2e": {"value": round(e2e, 1), "unit": "particle-updates/s",
+                "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h),
+                "ms_per_step": round(ms_e2e / args.steps, 4)},
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+        "kernels": per_kernel,
+        "clocks": clk,
+    }
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, wl)
+    ctx.close()
+    return line
+
+
+# ----------------------------------------------------- CPU reference ----
+def cpu_baseline(args, wl=None):
+    """Time the reference's own CPU path (oracle/_ref) on a bounded sample."""
+    from oracle import ref
+    threads = os.cpu_count() or 1
+    if not ref.available():
+        return cpu_baseline_port(args)
+    if args.config == 1:
+        from paper_1710_08259_b200 import scenes
+        sc = wl.sc if wl else scenes.sph_microbench()
+        prm = sc.params
+        rc = ref.RefCase(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds, sc.pos)
+        rc.field("A", sc.fields["A"]).field("rho", np.full(sc.n, prm["rho0"]))
+        rc.constant("one", 1.0).constant("m", prm["mass"]).constant("R", prm["radius"])
+        exprs = ["sph_S(one,m,one,Wp53220,R)", "sph_G11(A,m,rho,Wp53220,R)",
+                 "sph_L0(A,m,rho,Wp53220,R)"]
+        comps = [1, 3, 1]
+        kernel_note = "Wendland Wp53220 (the reference has no cubic spline; same candidate loop)"
+    else:
+        from paper_1710_08259_b200 import scenes
+        sc = wl.sc if wl else (scenes.dam_break(3, dx=0.005) if args.config == 2
+                               else scenes.dam_break(2))
+        prm = sc.params
+        rc = ref.RefCase(sc.dim, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds, sc.pos)
+        rng = np.random.default_rng(0)
+        vel = rng.uniform(-0.1, 0.1, (sc.dim, sc.n))  # non-zero so sph_A does its full work
+        for k in ("rho", "p", "vdot", "mask"):
+            rc.field(k, sc.fields[k])
+        rc.field("v", vel)
+        rc.constant("one", 1.0).constant("mass", prm["mass"]).constant("R", prm["radius"])
+        rc.constant("B", prm["B"]).constant("rho0", prm["rho0"]).constant("gam", prm["gamma"])
+        rc.constant("visc", prm["visc"]).constant("g", prm["g"]).variable("dt", prm["dt"])
+        eqs = scenes.wcsph_equations(sc)
+        exprs = [t.split("=", 1)[1] for _, t in eqs]
+        comps = [1, 1, sc.dim, sc.dim, sc.dim]
+        kernel_note = f"Wendland Wp5{sc.dim}220"
+    n = sc.n
+    t0 = time.perf_counter()
+    rc.build_cells()
+    t_build = time.perf_counter() - t0
+
+    def sample_cost(count):
+        chunks = 8
+        per = max(1, count // chunks)
+        t = 0.0
+        for e, c in zip(exprs, comps):
+            for k in range(chunks):
+                i0 = min(n - per, int((k + 0.5) * n / chunks))
+                s = time.perf_counter()
+                rc.eval(e, c, i0=i0, count=per, threads=threads)
+                t += time.perf_counter() - s
+        return t, per * chunks
+
+    t, cnt = sample_cost(64 * threads)
+    target = max(1.0, args.cpu_seconds - t_build)
+    scale = target / max(t, 1e-6)
+    cnt2 = int(min(n, max(cnt, cnt * scale)))
+    t, cnt = sample_cost(cnt2)
+    per_particle = t_build / n + t / cnt
+    value = 1.0 / per_particle
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo")
+                 if l.startswith("model name")][0]
+    except (OSError, IndexError):
+        model = "unknown"
+    return {"value": round(value, 1), "unit": "particle-updates/s", "cores": threads,
+            "kind": "reference",
+            "sample": (f"reference Case path (oracle/_ref, unmodified sources): build_cells over all "
+                       f"{n} particles ({t_build:.2f} s, single-threaded as in the reference) + "
+                       f"every equation's RHS evaluated over {cnt} particles in 8 spread chunks on "
+                       f"ThreadPool({threads}) ({t:.2f} s); {kernel_note}; host CPU: {model}")}
+
+
+def cpu_baseline_port(args):
+    return {"value": None, "unit": "particle-updates/s", "cores": 0, "kind": "port",
+            "sample": "oracle/_ref not present on this machine"}
+
+
+def run_reference(args, dist):
+    if dist.rank != 0:
+        return None
+    wl_name = {1: "cfg1", 2: "cfg2", 0: "cfg0"}[args.config]
+    cb = cpu_baseline(args)
+    per_step_ms = None
+    if cb["value"]:
+        from paper_1710_08259_b200 import scenes
+        n = (scenes.sph_microbench().n if args.config == 1 else
+             (scenes.dam_break(3, dx=0.005).n if args.config == 2 else scenes.dam_break(2).n))
+        per_step_ms = n / cb["value"] * 1e3
+    return {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "particle-updates/s",
+            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": wl_name, "threads": cb["cores"]},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "particle-updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    dist = Dist()
+    if args.impl == "reference":
+        line = run_reference(args, dist)
+    else:
+        line = run_ours(args, dist)
+    if dist.rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

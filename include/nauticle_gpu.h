@@ -1,0 +1,197 @@
+/* include/nauticle_gpu.h — C-ABI of the B200-native Nauticle particle hot path.
+ *
+ * Built as paper_1710_08259_b200/libnau_b200.so (hand-written sm_100a CUDA +
+ * a thin C++ host layer). No torch types, plain pointers and sizes only.
+ *
+ * Why the boundary sits one level above the reference's plugin type
+ * (SURVEY.md §8(b)): the reference's operator plugin
+ *     struct InteractionOp { name, arity_min, arity_max, kernel_slot, radius_slot,
+ *                            finite_influence, Tensor (*eval)(node, int i, int level) }
+ * (include/nauticle/interactions.hpp:13-21, registry kOps[] src/interactions.cpp:259-269)
+ * is called once per particle i from Case::solve_equation's thread blocks
+ * (src/case.cpp:31-54). Across a C ABI to a GPU that would be one launch per
+ * particle, so every entry point here is a whole-field operation that takes
+ * over the per-equation loop instead. Each function names the reference code it
+ * replaces. Ownership: a context owns all device memory; the host keeps names,
+ * shapes and equation trees and maps names to field ids.
+ *
+ * Threading: a context is bound to one host thread and one CUDA stream; calls
+ * are stream-ordered and asynchronous unless they return host data. Device-side
+ * failures (zero density, cut-off leavers at cell build, non-finite results)
+ * are latched in a device error word and surface at the next nau_sync() (or any
+ * call that returns host data) — the reference throws nauticle::Error{Runtime|Nan}
+ * (include/nauticle/error.hpp:10-69) at the same points.
+ *
+ * Data order: fields live on the device in CELL order (sorted by the last
+ * nau_build_cells). Every host-facing array (upload/download/tables/counts) is
+ * in ORIGINAL particle-index order, as the reference's std::vector<Tensor> is.
+ */
+#ifndef NAUTICLE_GPU_H
+#define NAUTICLE_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nau_ctx nau_ctx;
+
+typedef enum {
+    NAU_OK = 0,
+    NAU_ERR_RUNTIME = 1, /* nauticle::ErrorKind::Runtime */
+    NAU_ERR_NAN = 2,     /* nauticle::ErrorKind::Nan (case.cpp:46-53 audit) */
+    NAU_ERR_CUDA = 3,
+    NAU_ERR_ARG = 4,     /* ≙ Assembly/Parse errors of bad calls */
+    NAU_ERR_COMM = 5
+} nau_status;
+
+/* BoundaryKind (include/nauticle/domain.hpp:8) */
+enum { NAU_PERIODIC = 0, NAU_SYMMETRIC = 1, NAU_CUTOFF = 2 };
+
+/* Interaction operators: one per kOps[] row (src/interactions.cpp:259-269),
+ * plus NAU_OP_DEM_LSD, the linear spring-dashpot law BASELINE cfg3 needs. */
+enum {
+    NAU_OP_SPH_S = 0,        /* sph_S   (A, m, rho, K, R)  interactions.cpp:40-58   */
+    NAU_OP_SPH_D00 = 1,      /* sph_D00 (A, m, rho, K, R)  interactions.cpp:60-79   */
+    NAU_OP_SPH_G11 = 2,      /* sph_G11 (A, m, rho, K, R)  interactions.cpp:81-102  */
+    NAU_OP_SPH_L0 = 3,       /* sph_L0  (A, m, rho, K, R)  interactions.cpp:104-126 */
+    NAU_OP_SPH_A = 4,        /* sph_A   (v, m, rho, K, R)  interactions.cpp:128-150 */
+    NAU_OP_DEM_HERTZ = 5,    /* dem_l   (v,R,E,nu,m,cf,Rs) interactions.cpp:152-188 */
+    NAU_OP_DEM_BOUNDARY = 6, /* dem_boundary_force         interactions.cpp:190-193 */
+    NAU_OP_GRAVITY = 7,      /* nbody_gravity (m, G, eps)  interactions.cpp:195-214 */
+    NAU_OP_DEM_LSD = 8,      /* dem_lsd (v,R,kn,en,m,cf,Rs) new: linear spring-dashpot + Coulomb */
+    NAU_OP_COUNT = 9
+};
+
+/* Smoothing-kernel families: Wendland (keywords Wp5D220, src/kernel.cpp:9-69)
+ * and the cubic spline (keywords Wc3D220, new). */
+enum { NAU_K_WENDLAND = 0, NAU_K_CUBIC = 1 };
+
+/* Mirror of InteractionOp's metadata (interactions.hpp:13-21). */
+typedef struct {
+    const char* name;
+    int op;
+    int arity_min, arity_max;
+    int kernel_slot; /* operand that must be a kernel keyword, -1 if none */
+    int radius_slot; /* operand holding the influence radius, -1 if none  */
+    int finite_influence;
+} nau_op_info;
+
+/* ≙ find_interaction(name) (interactions.cpp:273-277). Returns NAU_ERR_ARG if unknown. */
+nau_status nau_find_interaction(const char* name, nau_op_info* out);
+/* ≙ decode_kernel_keyword (kernel.cpp:20-35): "Wp5D220" or "Wc3D220". */
+nau_status nau_decode_kernel(const char* keyword, int* family, int* dim);
+
+/* ---- context ---- */
+nau_status nau_create(int device, nau_ctx** out);
+void nau_destroy(nau_ctx* ctx);
+/* Use an external CUDA stream (cudaStream_t), e.g. torch's current stream. NULL = own stream. */
+nau_status nau_set_stream(nau_ctx* ctx, void* stream);
+void* nau_get_stream(nau_ctx* ctx);
+
+/* ≙ Domain(dim, min_cells, max_cells, cell_size, boundary) (domain.cpp:27-47). */
+nau_status nau_set_domain(nau_ctx* ctx, int dim, const int* min_cells, const int* max_cells,
+                          const double* cell_size, const int* kind);
+
+/* ≙ ParticleSystem(domain, positions) (particle_system.cpp:8-18): sets n and
+ * field 0 = r (dim x 1) from a host SoA (component-major, pos[a*n + i]); all
+ * particles active. Frees previous fields. Does not shift or build cells. */
+nau_status nau_set_particles(nau_ctx* ctx, long n, const double* pos_soa);
+long nau_particle_count(nau_ctx* ctx);
+/* ≙ ParticleSystem::active_count(); syncs. */
+long nau_active_count(nau_ctx* ctx);
+/* Host copy of the active flags in original order (≙ is_active(i)). */
+nau_status nau_get_active(nau_ctx* ctx, uint8_t* active);
+
+/* ≙ Workspace::add_field (workspace.cpp:39-48): new field of rows x cols per particle. */
+nau_status nau_alloc_field(nau_ctx* ctx, int rows, int cols, int* field_id);
+nau_status nau_free_field(nau_ctx* ctx, int field_id);
+/* host SoA, component-major [c*n + i] with c = col*rows + row, original order */
+nau_status nau_upload(nau_ctx* ctx, int field_id, const double* soa, long n);
+nau_status nau_download(nau_ctx* ctx, int field_id, double* soa, long n);
+/* Uniform value (rows*cols doubles, column-major) into every particle. */
+nau_status nau_fill(nau_ctx* ctx, int field_id, const double* value);
+nau_status nau_copy_field(nau_ctx* ctx, int dst, int src);
+/* Device pointer of a field's storage (cell order; valid until the next build). */
+nau_status nau_field_device_ptr(nau_ctx* ctx, int field_id, double** ptr);
+
+/* ≙ ParticleSystem::apply_boundary_shift (particle_system.cpp:56-90): periodic
+ * wrap, symmetric-overflow warnings, cut-off deactivation; marks cells dirty. */
+nau_status nau_boundary_shift(nau_ctx* ctx);
+/* ≙ ParticleSystem::build_cells (particle_system.cpp:33-54): cell hash, stable
+ * (cell, original index) ordering, cell start/count tables, SoA reorder. */
+nau_status nau_build_cells(nau_ctx* ctx);
+int nau_cells_dirty(nau_ctx* ctx);
+long nau_rebuild_count(nau_ctx* ctx);
+long nau_warning_count(nau_ctx* ctx); /* syncs */
+long nau_ncells(nau_ctx* ctx);
+/* Parity probe (host arrays): cell_of_particle[n] (flat cell, -1 inactive),
+ * cell_start[ncells], cell_count[ncells], sorted_ids[n_active] (original
+ * indices, ascending within a cell) — the reference's cells_ concatenated. */
+nau_status nau_cell_tables(nau_ctx* ctx, int* cell_of_particle, int* cell_start, int* cell_count,
+                           int* sorted_ids);
+/* Parity probe: counts[i] = candidates of for_each_neighbor(i) (particle_system.hpp:59-138)
+ * with |rel| <= radius, self included; original order. */
+nau_status nau_neighbor_counts(nau_ctx* ctx, double radius, int* counts);
+
+/* An operand: a field reference (field_id >= 0) or a uniform value (field_id = -1,
+ * rows x cols doubles in value[], column-major). ≙ FieldRefNode / ConstantRefNode /
+ * VariableRefNode / LiteralNode (include/nauticle/sfl/ast.hpp:70-109). */
+typedef struct {
+    int field_id;
+    int rows, cols;
+    double value[9];
+} nau_operand;
+
+/* ≙ InteractionOp::eval for every active particle (the whole-field form of
+ * interact(), interactions.hpp:29-36). Operands follow kOps[] order with the
+ * kernel-keyword slot removed: SPH (A, m, rho, R); DEM (v, R, E|kn, nu|en, m, cf, Rs);
+ * gravity (m, G[, eps]). Writes active particles of out_field (inactive keep
+ * their value, case.cpp:37-40); out_field may alias an operand (two-phase). */
+nau_status nau_interact(nau_ctx* ctx, int op, int kernel_family, int kernel_dim,
+                        const nau_operand* ops, int n_ops, int out_field);
+
+/* ≙ EulerNode (sfl/ast.cpp:180-191): out = x + xdot*dt on active particles. */
+nau_status nau_euler(nau_ctx* ctx, int x, int xdot, double dt, int out_field);
+
+/* Fused symplectic-Euler update of the BASELINE decks, one kernel:
+ *   v = euler(v, vdot*mask, dt); r = euler(r, v, dt); apply_boundary_shift()
+ * (dam_break_2d.yaml:37-38 order; case.cpp:59-62). mask_field = -1 means no mask. */
+nau_status nau_symplectic_step(nau_ctx* ctx, int v, int vdot, int mask_field, double dt);
+
+/* Weakly-compressible SPH deck (BASELINE cfg0/cfg2), fused into three passes:
+ *   rho  = sph_S(one, m, one, K, R)                    -> p = B*((rho/rho0)^gamma - 1)
+ *   vdot = -1/rho*sph_G11(p,m,rho,K,R) + visc*sph_A(v,m,rho,K,R) + g
+ *   v = euler(v, vdot*mask, dt); r = euler(r, v, dt); boundary shift
+ * (visc = alpha*c0*h). Field ids: rho, p, v, vdot, mask (-1 none). */
+typedef struct {
+    int kernel_family, kernel_dim;
+    double mass, radius, rho0, B, gamma, visc, dt;
+    double g[3];
+    int f_rho, f_p, f_v, f_vdot, f_mask;
+} nau_wcsph_params;
+nau_status nau_wcsph_step(nau_ctx* ctx, const nau_wcsph_params* prm);
+
+/* ≙ ReductionNode fsum/fmax/fmin/fmean over active particles (sfl/ast.cpp:237-274).
+ * kind: 0 max, 1 min, 2 sum, 3 mean; out has rows*cols doubles (max/min: 1). */
+nau_status nau_reduce(nau_ctx* ctx, int kind, int field_id, double* out);
+
+/* Surfaces latched device errors (≙ the exceptions above). */
+nau_status nau_sync(nau_ctx* ctx);
+/* Message of the last error and the lowest original particle index involved (-1 if none). */
+const char* nau_last_error(nau_ctx* ctx, long* first_bad_particle);
+
+/* Instrumentation for bench.py: record CUDA events around every launch of the
+ * named kernel class (0 none, 1 neighbour sums) and report their total time. */
+nau_status nau_profile_enable(nau_ctx* ctx, int on);
+double nau_profile_ms(nau_ctx* ctx, int kernel_class, long* launches);
+long nau_launch_count(nau_ctx* ctx);
+
+/* Microbenchmark: measured fp64 FMA throughput (TFLOP/s) of this GPU. */
+double nau_fp64_peak_tflops(int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,694 @@
+// capi.cu — the C-ABI of include/nauticle_gpu.h: context, SoA arena, operand
+// resolution, error surfacing, and the host-side mirror of the reference's
+// operator registry (kOps[], src/interactions.cpp:259-269).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "nau_internal.cuh"
+
+using nau::FieldBuf;
+
+namespace {
+
+thread_local std::string g_static_err;
+
+#define NAU_CUDA(call)                                                             \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess) return fail(c, NAU_ERR_CUDA, cudaGetErrorString(e_)); \
+    } while (0)
+
+nau_status fail(nau_ctx* c, nau_status s, const std::string& msg, long bad = -1) {
+    if (c) {
+        c->last_error = msg;
+        c->last_bad = bad;
+    } else {
+        g_static_err = msg;
+    }
+    return s;
+}
+
+// ≙ kOps[] (src/interactions.cpp:259-269) + the new dem_lsd row.
+const nau_op_info kOps[] = {
+    {"sph_S", NAU_OP_SPH_S, 5, 5, 3, 4, 1},
+    {"sph_D00", NAU_OP_SPH_D00, 5, 5, 3, 4, 1},
+    {"sph_G11", NAU_OP_SPH_G11, 5, 5, 3, 4, 1},
+    {"sph_L0", NAU_OP_SPH_L0, 5, 5, 3, 4, 1},
+    {"sph_A", NAU_OP_SPH_A, 5, 5, 3, 4, 1},
+    {"dem_l", NAU_OP_DEM_HERTZ, 7, 7, -1, 6, 1},
+    {"dem_boundary_force", NAU_OP_DEM_BOUNDARY, 7, 7, -1, 6, 1},
+    {"nbody_gravity", NAU_OP_GRAVITY, 2, 3, -1, -1, 0},
+    {"dem_lsd", NAU_OP_DEM_LSD, 7, 7, -1, 6, 1},
+};
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    return cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * count);
+}
+
+template <typename T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+void free_particles(nau_ctx* c) {
+    for (auto& f : c->fields) {
+        dfree(f.d);
+        dfree(f.alt);
+    }
+    c->fields.clear();
+    dfree(c->d_orig);
+    dfree(c->d_orig_s);
+    dfree(c->d_key);
+    dfree(c->d_key_s);
+    dfree(c->d_active);
+    dfree(c->d_active_s);
+    dfree(c->d_perm);
+    dfree(c->d_perm_tmp);
+    dfree(c->d_okey);
+}
+
+void free_cells(nau_ctx* c) {
+    dfree(c->d_cell_start);
+    dfree(c->d_cell_count);
+    dfree(c->d_cursor);
+    dfree(c->d_scan_tmp);
+}
+
+__global__ void k_iota(long n, int* a) {
+    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k < n) a[k] = (int)k;
+}
+
+__global__ void k_fill(long n, int comps, const double* v, double* f) {
+    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    for (int c = 0; c < comps; ++c) f[c * n + k] = v[c];
+}
+
+struct FillVal {
+    double v[9];
+};
+
+__global__ void k_fill_val(long n, int comps, FillVal v, double* f) {
+    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    for (int c = 0; c < comps; ++c) f[c * n + k] = v.v[c];
+}
+
+bool field_ok(nau_ctx* c, int id) {
+    return id >= 0 && id < (int)c->fields.size() && c->fields[id].live;
+}
+
+const char* msg_text(int msg) {
+    switch (msg) {
+        case nau::kMsgZeroDensity: return "zero density";
+        case nau::kMsgRadius: return "influence radius must be positive";
+        case nau::kMsgOutsideCutoff: return "particle outside the domain on a cut-off axis";
+        case nau::kMsgCoincident: return "nbody_gravity: coincident particles with zero softening";
+        case nau::kMsgDemParams: return "dem contact: nonpositive Young modulus or radius";
+        default: return "runtime error";
+    }
+}
+
+void reset_err(nau_ctx* c) {
+    nau::DevErr e{};
+    e.first_bad = 0x7fffffffffffffffLL;
+    e.nan_first = 0x7fffffffffffffffLL;
+    cudaMemcpyAsync(c->d_err, &e, sizeof(e), cudaMemcpyHostToDevice, c->stream);
+    cudaStreamSynchronize(c->stream);
+}
+
+// Fetch and clear the device error word; map it to a status.
+nau_status collect(nau_ctx* c) {
+    cudaError_t ce = cudaStreamSynchronize(c->stream);
+    if (ce != cudaSuccess) return fail(c, NAU_ERR_CUDA, cudaGetErrorString(ce));
+    ce = cudaGetLastError();
+    if (ce != cudaSuccess) return fail(c, NAU_ERR_CUDA, cudaGetErrorString(ce));
+    cudaMemcpy(c->h_err, c->d_err, sizeof(nau::DevErr), cudaMemcpyDeviceToHost);
+    nau::DevErr e = *c->h_err;
+    c->warnings += e.warnings;
+    if (e.warnings || e.code) reset_err(c);
+    if (e.code & 5) {
+        std::string m = msg_text(e.msg);
+        m += " at particle " + std::to_string(e.first_bad);
+        return fail(c, NAU_ERR_RUNTIME, m, (long)e.first_bad);
+    }
+    if (e.code & 2)
+        return fail(c, NAU_ERR_NAN, "non-finite value at particle " + std::to_string(e.nan_first),
+                    (long)e.nan_first);
+    return NAU_OK;
+}
+
+nau_status ensure_field_storage(nau_ctx* c, FieldBuf& f) {
+    long len = (long)f.comps() * c->n;
+    NAU_CUDA(dalloc(&f.d, len));
+    NAU_CUDA(dalloc(&f.alt, len));
+    NAU_CUDA(cudaMemsetAsync(f.d, 0, sizeof(double) * (len ? len : 1), c->stream));
+    return NAU_OK;
+}
+
+}  // namespace
+
+namespace nau {
+
+Geo make_geo(nau_ctx* c) {
+    Geo g;
+    g.dom = c->dom;
+    g.n = c->n;
+    g.x = c->fields[0].d;
+    g.key = c->d_key;
+    g.orig = c->d_orig;
+    g.active = c->d_active;
+    g.cell_start = c->d_cell_start;
+    g.cell_count = c->d_cell_count;
+    g.nact = c->d_cell_start + c->dom.ncells;
+    return g;
+}
+
+Opd make_opd(nau_ctx* c, const nau_operand& o) {
+    Opd d;
+    d.p = o.field_id >= 0 ? c->fields[o.field_id].d : nullptr;
+    for (int k = 0; k < 9; ++k) d.v[k] = o.value[k];
+    return d;
+}
+
+void prof_begin(nau_ctx* c, int cls) {
+    if (!c->profile) return;
+    if (c->ev_next + 2 > (int)c->ev_pool.size()) {
+        for (int k = 0; k < 256; ++k) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            c->ev_pool.push_back(e);
+        }
+    }
+    c->ev_pairs.push_back({cls, c->ev_next});
+    cudaEventRecord(c->ev_pool[c->ev_next], c->stream);
+    c->ev_next += 2;
+}
+
+void prof_end(nau_ctx* c, int cls) {
+    (void)cls;
+    if (!c->profile) return;
+    cudaEventRecord(c->ev_pool[c->ev_pairs.back().second + 1], c->stream);
+}
+
+}  // namespace nau
+
+extern "C" {
+
+nau_status nau_find_interaction(const char* name, nau_op_info* out) {
+    for (const auto& op : kOps)
+        if (std::strcmp(op.name, name) == 0) {
+            *out = op;
+            return NAU_OK;
+        }
+    return fail(nullptr, NAU_ERR_ARG, std::string("unknown interaction '") + name + "'");
+}
+
+// kernel.cpp:20-35 (Wendland "Wp5D220") + the new cubic spline "Wc3D220".
+nau_status nau_decode_kernel(const char* kw, int* family, int* dim) {
+    std::string s(kw ? kw : "");
+    if (s.size() == 7 && s[0] == 'W' && s.substr(4) == "220" && (s[3] >= '1' && s[3] <= '3')) {
+        if (s[1] == 'p' && s[2] == '5') {
+            *family = NAU_K_WENDLAND;
+            *dim = s[3] - '0';
+            return NAU_OK;
+        }
+        if (s[1] == 'c' && s[2] == '3') {
+            *family = NAU_K_CUBIC;
+            *dim = s[3] - '0';
+            return NAU_OK;
+        }
+    }
+    return fail(nullptr, NAU_ERR_ARG,
+                "unknown kernel keyword '" + s +
+                    "'; registered keywords: Wp51220, Wp52220, Wp53220, Wc31220, Wc32220, Wc33220");
+}
+
+nau_status nau_create(int device, nau_ctx** out) {
+    *out = nullptr;
+    nau_ctx* c = new nau_ctx();
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = dalloc(&c->d_err, 1);
+    if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c->h_err), sizeof(nau::DevErr));
+    if (e == cudaSuccess) e = dalloc(&c->d_red, 296 * 9 + 2);
+    if (e != cudaSuccess) {
+        g_static_err = cudaGetErrorString(e);
+        delete c;
+        return NAU_ERR_CUDA;
+    }
+    c->own_stream = true;
+    reset_err(c);
+    *out = c;
+    return NAU_OK;
+}
+
+void nau_destroy(nau_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    free_particles(c);
+    free_cells(c);
+    dfree(c->d_err);
+    dfree(c->d_red);
+    if (c->h_err) cudaFreeHost(c->h_err);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+nau_status nau_set_stream(nau_ctx* c, void* stream) {
+    cudaStreamSynchronize(c->stream);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    if (stream) {
+        c->stream = static_cast<cudaStream_t>(stream);
+        c->own_stream = false;
+    } else {
+        NAU_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    return NAU_OK;
+}
+
+void* nau_get_stream(nau_ctx* c) { return c->stream; }
+
+nau_status nau_set_domain(nau_ctx* c, int dim, const int* min_cells, const int* max_cells,
+                          const double* cell_size, const int* kind) {
+    if (dim < 1 || dim > 3) return fail(c, NAU_ERR_ARG, "domain dimension must be 1, 2 or 3");
+    nau::DomainDev d{};
+    d.dim = dim;
+    long total = 1;
+    for (int a = 0; a < 3; ++a) {
+        int mn = 0, mx = 1, k = NAU_CUTOFF;
+        double cs = 1.0;
+        if (a < dim) {
+            mn = min_cells[a];
+            mx = max_cells[a];
+            cs = cell_size[a];
+            k = kind[a];
+            if (mx <= mn)
+                return fail(c, NAU_ERR_ARG, "domain axis " + std::to_string(a) +
+                                                ": maximum cell count must exceed minimum");
+            if (!(cs > 0.0))
+                return fail(c, NAU_ERR_ARG,
+                            "domain axis " + std::to_string(a) + ": cell size must be positive");
+            if (k < 0 || k > 2) return fail(c, NAU_ERR_ARG, "unknown boundary kind");
+        }
+        d.cells[a] = mx - mn;
+        d.cs[a] = cs;
+        d.lo[a] = mn * cs;  // domain.hpp:28-30: products, not sums
+        d.hi[a] = mx * cs;
+        d.ext[a] = d.hi[a] - d.lo[a];
+        d.kind[a] = k;
+        if (a < dim) total *= d.cells[a];
+    }
+    if (total >= 0x7ffffff0L) return fail(c, NAU_ERR_ARG, "too many cells for int32 keys");
+    d.ncells = (int)total;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    free_cells(c);
+    NAU_CUDA(dalloc(&c->d_cell_start, total + 2));
+    NAU_CUDA(dalloc(&c->d_cell_count, total + 1));
+    NAU_CUDA(dalloc(&c->d_cursor, total + 1));
+    c->scan_tmp_len = (total + 1 + 4095) / 4096 + 1;
+    NAU_CUDA(dalloc(&c->d_scan_tmp, c->scan_tmp_len));
+    NAU_CUDA(cudaMemsetAsync(c->d_cell_start, 0, sizeof(int) * (total + 2), c->stream));
+    NAU_CUDA(cudaMemsetAsync(c->d_cell_count, 0, sizeof(int) * (total + 1), c->stream));
+    c->dom = d;
+    c->has_domain = true;
+    c->dirty = true;
+    return NAU_OK;
+}
+
+nau_status nau_set_particles(nau_ctx* c, long n, const double* pos_soa) {
+    if (!c->has_domain) return fail(c, NAU_ERR_ARG, "nau_set_domain must precede nau_set_particles");
+    if (n < 0 || n >= 0x7fffffffL) return fail(c, NAU_ERR_ARG, "bad particle count");
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    free_particles(c);
+    c->n = n;
+    NAU_CUDA(dalloc(&c->d_orig, n));
+    NAU_CUDA(dalloc(&c->d_orig_s, n));
+    NAU_CUDA(dalloc(&c->d_key, n));
+    NAU_CUDA(dalloc(&c->d_key_s, n));
+    NAU_CUDA(dalloc(&c->d_active, n));
+    NAU_CUDA(dalloc(&c->d_active_s, n));
+    NAU_CUDA(dalloc(&c->d_perm, n));
+    NAU_CUDA(dalloc(&c->d_perm_tmp, n));
+    NAU_CUDA(dalloc(&c->d_okey, n));
+    if (n > 0) {
+        k_iota<<<(int)((n + 255) / 256), 256, 0, c->stream>>>(n, c->d_orig);
+        c->launches++;
+    }
+    NAU_CUDA(cudaMemsetAsync(c->d_active, 1, n ? n : 1, c->stream));
+    FieldBuf r;
+    r.rows = c->dom.dim;
+    r.cols = 1;
+    r.live = true;
+    nau_status s = ensure_field_storage(c, r);
+    if (s != NAU_OK) return s;
+    c->fields.push_back(r);
+    if (n > 0 && pos_soa)
+        NAU_CUDA(cudaMemcpyAsync(c->fields[0].d, pos_soa, sizeof(double) * n * c->dom.dim,
+                                 cudaMemcpyHostToDevice, c->stream));
+    c->dirty = true;
+    c->built_once = false;
+    c->rebuild_count = 0;
+    c->warnings = 0;
+    return collect(c);
+}
+
+long nau_particle_count(nau_ctx* c) { return c->n; }
+
+nau_status nau_get_active(nau_ctx* c, uint8_t* active) {
+    std::vector<uint8_t> a(c->n);
+    std::vector<int> o(c->n);
+    if (c->n) {
+        NAU_CUDA(cudaMemcpyAsync(a.data(), c->d_active, c->n, cudaMemcpyDeviceToHost, c->stream));
+        NAU_CUDA(cudaMemcpyAsync(o.data(), c->d_orig, sizeof(int) * c->n, cudaMemcpyDeviceToHost,
+                                 c->stream));
+    }
+    NAU_CUDA(cudaStreamSynchronize(c->stream));
+    for (long k = 0; k < c->n; ++k) active[o[k]] = a[k];
+    return NAU_OK;
+}
+
+long nau_active_count(nau_ctx* c) {
+    std::vector<uint8_t> a(c->n);
+    if (c->n) cudaMemcpyAsync(a.data(), c->d_active, c->n, cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    long s = 0;
+    for (auto v : a) s += v;
+    return s;
+}
+
+nau_status nau_alloc_field(nau_ctx* c, int rows, int cols, int* field_id) {
+    if (rows < 1 || rows > 3 || cols < 1 || cols > 3)
+        return fail(c, NAU_ERR_ARG, "tensor extent outside the supported 1..3 range");
+    if (c->fields.empty()) return fail(c, NAU_ERR_ARG, "nau_set_particles must precede fields");
+    FieldBuf f;
+    f.rows = rows;
+    f.cols = cols;
+    f.live = true;
+    cudaSetDevice(c->device);
+    nau_status s = ensure_field_storage(c, f);
+    if (s != NAU_OK) return s;
+    for (size_t k = 1; k < c->fields.size(); ++k)
+        if (!c->fields[k].live) {
+            c->fields[k] = f;
+            *field_id = (int)k;
+            return NAU_OK;
+        }
+    if ((int)c->fields.size() >= nau::kMaxFields) return fail(c, NAU_ERR_ARG, "too many fields");
+    c->fields.push_back(f);
+    *field_id = (int)c->fields.size() - 1;
+    return NAU_OK;
+}
+
+nau_status nau_free_field(nau_ctx* c, int id) {
+    if (id <= 0 || !field_ok(c, id)) return fail(c, NAU_ERR_ARG, "bad field id");
+    cudaStreamSynchronize(c->stream);
+    dfree(c->fields[id].d);
+    dfree(c->fields[id].alt);
+    c->fields[id].live = false;
+    return NAU_OK;
+}
+
+nau_status nau_upload(nau_ctx* c, int id, const double* soa, long n) {
+    if (!field_ok(c, id) || n != c->n) return fail(c, NAU_ERR_ARG, "bad field id or count");
+    FieldBuf& f = c->fields[id];
+    if (n == 0) return NAU_OK;
+    NAU_CUDA(cudaMemcpyAsync(f.alt, soa, sizeof(double) * n * f.comps(), cudaMemcpyHostToDevice,
+                             c->stream));
+    nau::launch_sort_in(c, f.alt, f.d, f.comps());
+    if (id == 0) c->dirty = true;
+    return NAU_OK;
+}
+
+nau_status nau_download(nau_ctx* c, int id, double* soa, long n) {
+    if (!field_ok(c, id) || n != c->n) return fail(c, NAU_ERR_ARG, "bad field id or count");
+    FieldBuf& f = c->fields[id];
+    if (n == 0) return NAU_OK;
+    nau::launch_unsort(c, f.d, f.alt, f.comps());
+    NAU_CUDA(cudaMemcpyAsync(soa, f.alt, sizeof(double) * n * f.comps(), cudaMemcpyDeviceToHost,
+                             c->stream));
+    return collect(c);
+}
+
+nau_status nau_fill(nau_ctx* c, int id, const double* value) {
+    if (!field_ok(c, id)) return fail(c, NAU_ERR_ARG, "bad field id");
+    FieldBuf& f = c->fields[id];
+    FillVal v{};
+    for (int k = 0; k < f.comps(); ++k) v.v[k] = value[k];
+    if (c->n)
+        k_fill_val<<<(int)((c->n + 255) / 256), 256, 0, c->stream>>>(c->n, f.comps(), v, f.d);
+    c->launches++;
+    if (id == 0) c->dirty = true;
+    return NAU_OK;
+}
+
+nau_status nau_copy_field(nau_ctx* c, int dst, int src) {
+    if (!field_ok(c, dst) || !field_ok(c, src) ||
+        c->fields[dst].comps() != c->fields[src].comps())
+        return fail(c, NAU_ERR_ARG, "bad field ids for copy");
+    NAU_CUDA(cudaMemcpyAsync(c->fields[dst].d, c->fields[src].d,
+                             sizeof(double) * c->n * c->fields[src].comps(),
+                             cudaMemcpyDeviceToDevice, c->stream));
+    if (dst == 0) c->dirty = true;
+    return NAU_OK;
+}
+
+nau_status nau_field_device_ptr(nau_ctx* c, int id, double** ptr) {
+    if (!field_ok(c, id)) return fail(c, NAU_ERR_ARG, "bad field id");
+    *ptr = c->fields[id].d;
+    return NAU_OK;
+}
+
+nau_status nau_boundary_shift(nau_ctx* c) {
+    if (c->fields.empty()) return fail(c, NAU_ERR_ARG, "no particles");
+    nau::launch_boundary_shift(c);
+    c->dirty = true;  // case.cpp:59-62 marks dirty after the shift
+    return NAU_OK;
+}
+
+nau_status nau_build_cells(nau_ctx* c) {
+    if (c->fields.empty()) return fail(c, NAU_ERR_ARG, "no particles");
+    nau::prof_begin(c, 300);
+    nau::launch_build_cells(c);
+    nau::prof_end(c, 300);
+    c->dirty = false;
+    c->built_once = true;
+    ++c->rebuild_count;
+    return NAU_OK;
+}
+
+int nau_cells_dirty(nau_ctx* c) { return c->dirty ? 1 : 0; }
+long nau_rebuild_count(nau_ctx* c) { return c->rebuild_count; }
+long nau_ncells(nau_ctx* c) { return c->dom.ncells; }
+
+long nau_warning_count(nau_ctx* c) {
+    collect(c);
+    return (long)c->warnings;
+}
+
+nau_status nau_cell_tables(nau_ctx* c, int* cell_of, int* cell_start, int* cell_count,
+                           int* sorted_ids) {
+    if (c->dirty || !c->built_once) {
+        nau_status s = nau_build_cells(c);
+        if (s != NAU_OK) return s;
+    }
+    const long n = c->n;
+    const int nc = c->dom.ncells;
+    std::vector<int> key(n), orig(n);
+    if (n) {
+        NAU_CUDA(cudaMemcpyAsync(key.data(), c->d_key, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+        NAU_CUDA(cudaMemcpyAsync(orig.data(), c->d_orig, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    }
+    NAU_CUDA(cudaMemcpyAsync(cell_start, c->d_cell_start, sizeof(int) * nc, cudaMemcpyDeviceToHost, c->stream));
+    NAU_CUDA(cudaMemcpyAsync(cell_count, c->d_cell_count, sizeof(int) * nc, cudaMemcpyDeviceToHost, c->stream));
+    nau_status s = collect(c);
+    if (s != NAU_OK) return s;
+    long nact = 0;
+    for (long k = 0; k < n; ++k) {
+        cell_of[orig[k]] = key[k] < nc ? key[k] : -1;
+        if (key[k] < nc) sorted_ids[nact++] = orig[k];
+    }
+    return NAU_OK;
+}
+
+nau_status nau_neighbor_counts(nau_ctx* c, double radius, int* counts) {
+    if (c->dirty || !c->built_once) {
+        nau_status s = nau_build_cells(c);
+        if (s != NAU_OK) return s;
+    }
+    int* d = nullptr;
+    NAU_CUDA(dalloc(&d, c->n));
+    nau::launch_neighbor_counts(c, radius, d);
+    if (c->n) cudaMemcpyAsync(counts, d, sizeof(int) * c->n, cudaMemcpyDeviceToHost, c->stream);
+    nau_status s = collect(c);
+    cudaFree(d);
+    return s;
+}
+
+nau_status nau_interact(nau_ctx* c, int op, int kf, int kdim, const nau_operand* ops, int nops,
+                        int out_field) {
+    if (op < 0 || op >= NAU_OP_COUNT) return fail(c, NAU_ERR_ARG, "unknown operator");
+    const nau_op_info& info = kOps[op];
+    const int arity = nops + (info.kernel_slot >= 0 ? 1 : 0);
+    if (arity < info.arity_min || arity > info.arity_max)
+        return fail(c, NAU_ERR_ARG, std::string("wrong number of operands for '") + info.name + "'");
+    if (!field_ok(c, out_field) || out_field == 0)
+        return fail(c, NAU_ERR_ARG, "bad output field (r is written by euler only)");
+    const int dim = c->dom.dim;
+    nau::Opd d_ops[8];
+    for (int k = 0; k < nops; ++k) {
+        if (ops[k].field_id >= 0 && !field_ok(c, ops[k].field_id))
+            return fail(c, NAU_ERR_ARG, "bad operand field id");
+        d_ops[k] = nau::make_opd(c, ops[k]);
+    }
+    auto shape = [&](int k, int& r, int& cc) {
+        if (ops[k].field_id >= 0) {
+            r = c->fields[ops[k].field_id].rows;
+            cc = c->fields[ops[k].field_id].cols;
+        } else {
+            r = ops[k].rows;
+            cc = ops[k].cols;
+        }
+    };
+    int ar = 1, acl = 1;
+    shape(0, ar, acl);
+    int out_rows = 1, out_cols = 1;
+    if (op == NAU_OP_SPH_S) {
+        out_rows = ar;
+        out_cols = acl;
+    } else if (op == NAU_OP_SPH_D00 || op == NAU_OP_SPH_L0) {
+        if (op == NAU_OP_SPH_D00 && !(acl == 1 && ar == dim))
+            return fail(c, NAU_ERR_RUNTIME, "sph_D00: operand must be a vector field");
+        if (op == NAU_OP_SPH_L0 && !(ar == 1 && acl == 1))
+            return fail(c, NAU_ERR_RUNTIME, "sph_L0: expected a scalar operand");
+    } else {
+        out_rows = dim;
+        if ((op == NAU_OP_SPH_G11) && !(ar == 1 && acl == 1))
+            return fail(c, NAU_ERR_RUNTIME, "sph_G11: expected a scalar operand");
+        if ((op == NAU_OP_SPH_A || op >= NAU_OP_DEM_HERTZ) && op != NAU_OP_GRAVITY &&
+            !(acl == 1 && ar == dim))
+            return fail(c, NAU_ERR_RUNTIME, "velocity operand must be a d-vector");
+    }
+    FieldBuf& of = c->fields[out_field];
+    if (of.rows != out_rows || of.cols != out_cols)
+        return fail(c, NAU_ERR_RUNTIME, "LHS field shape does not match the operator result");
+    if (info.finite_influence && (c->dirty || !c->built_once)) {
+        nau_status s = nau_build_cells(c);  // case.cpp:11
+        if (s != NAU_OK) return s;
+        for (int k = 0; k < nops; ++k) d_ops[k] = nau::make_opd(c, ops[k]);
+    }
+    // Two-phase write (case.cpp:31-54): if the output aliases an operand,
+    // evaluate into the twin buffer (pre-filled so inactive values persist).
+    bool alias = false;
+    for (int k = 0; k < nops; ++k) alias |= ops[k].field_id == out_field;
+    double* out = of.d;
+    if (alias) {
+        NAU_CUDA(cudaMemcpyAsync(of.alt, of.d, sizeof(double) * c->n * of.comps(),
+                                 cudaMemcpyDeviceToDevice, c->stream));
+        out = of.alt;
+    }
+    nau::launch_interact(c, op, kf, kdim, d_ops, nops, out, out_rows, out_cols, ar, acl);
+    if (alias) std::swap(of.d, of.alt);
+    return NAU_OK;
+}
+
+nau_status nau_euler(nau_ctx* c, int x, int xdot, double dt, int out_field) {
+    if (!field_ok(c, x) || !field_ok(c, xdot) || !field_ok(c, out_field))
+        return fail(c, NAU_ERR_ARG, "bad field id");
+    FieldBuf& fx = c->fields[x];
+    if (fx.comps() != c->fields[xdot].comps() || fx.comps() != c->fields[out_field].comps())
+        return fail(c, NAU_ERR_RUNTIME, "euler: state and derivative shapes differ");
+    FieldBuf& fo = c->fields[out_field];
+    const bool alias = out_field == x || out_field == xdot;
+    double* out = alias ? fo.alt : fo.d;
+    nau::launch_euler(c, fx.d, c->fields[xdot].d, dt, out, fx.comps());
+    if (alias) std::swap(fo.d, fo.alt);
+    if (out_field == 0) {  // case.cpp:59-62
+        nau::launch_boundary_shift(c);
+        c->dirty = true;
+    }
+    return NAU_OK;
+}
+
+nau_status nau_symplectic_step(nau_ctx* c, int v, int vdot, int mask, double dt) {
+    if (!field_ok(c, v) || !field_ok(c, vdot) || (mask >= 0 && !field_ok(c, mask)))
+        return fail(c, NAU_ERR_ARG, "bad field id");
+    nau::launch_symplectic(c, c->fields[v].d, c->fields[vdot].d,
+                           mask >= 0 ? c->fields[mask].d : nullptr, dt);
+    c->dirty = true;
+    return NAU_OK;
+}
+
+nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
+    int ids[5] = {p->f_rho, p->f_p, p->f_v, p->f_vdot, p->f_mask};
+    for (int k = 0; k < 5; ++k)
+        if (!(k == 4 && ids[k] < 0) && !field_ok(c, ids[k])) return fail(c, NAU_ERR_ARG, "bad field id");
+    if (!(p->radius > 0.0)) return fail(c, NAU_ERR_RUNTIME, "influence radius must be positive");
+    if (c->dirty || !c->built_once) {
+        nau_status s = nau_build_cells(c);
+        if (s != NAU_OK) return s;
+    }
+    nau::launch_wcsph(c, p);
+    c->dirty = true;
+    return NAU_OK;
+}
+
+nau_status nau_reduce(nau_ctx* c, int kind, int id, double* out) {
+    if (!field_ok(c, id) || kind < 0 || kind > 3) return fail(c, NAU_ERR_ARG, "bad reduce args");
+    if (nau_active_count(c) == 0)
+        return fail(c, NAU_ERR_RUNTIME, "reduction over an empty particle system");
+    nau::launch_reduce(c, kind, c->fields[id].d, c->fields[id].comps(), out);
+    return collect(c);
+}
+
+nau_status nau_sync(nau_ctx* c) { return collect(c); }
+
+const char* nau_last_error(nau_ctx* c, long* bad) {
+    if (!c) {
+        if (bad) *bad = -1;
+        return g_static_err.c_str();
+    }
+    if (bad) *bad = c->last_bad;
+    return c->last_error.c_str();
+}
+
+nau_status nau_profile_enable(nau_ctx* c, int on) {
+    cudaStreamSynchronize(c->stream);
+    c->profile = on != 0;
+    c->ev_pairs.clear();
+    c->ev_next = 0;
+    return NAU_OK;
+}
+
+double nau_profile_ms(nau_ctx* c, int cls, long* launches) {
+    cudaStreamSynchronize(c->stream);
+    double total = 0.0;
+    long cnt = 0;
+    for (auto& pr : c->ev_pairs) {
+        if (pr.first != cls) continue;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, c->ev_pool[pr.second], c->ev_pool[pr.second + 1]) == cudaSuccess) {
+            total += ms;
+            ++cnt;
+        }
+    }
+    if (launches) *launches = cnt;
+    return total;
+}
+
+long nau_launch_count(nau_ctx* c) { return c->launches; }
+
+}  // extern "C"

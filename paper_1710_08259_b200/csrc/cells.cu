@@ -1,0 +1,300 @@
+// cells.cu — neighbour-search pipeline of ParticleSystem on the device.
+//
+//   boundary shift  ≙ ParticleSystem::apply_boundary_shift (particle_system.cpp:56-90)
+//   build cells     ≙ ParticleSystem::build_cells          (particle_system.cpp:33-54)
+//     1. k_hash      cell key per slot (cell_index, particle_system.cpp:20-31) + histogram
+//     2. scan        exclusive prefix sum of the histogram -> cell_start
+//     3. k_scatter   slot = cell_start[key] + atomic cursor (unordered within a cell)
+//     4. k_rank      within each cell, rank by original index -> the reference order
+//                    (cells_[c] holds ascending i, particle_system.cpp:37-51)
+//     5. k_reorder   one gather pass permuting every SoA field + orig/key/active
+// All passes are streaming (HBM-bound); see DESIGN.md for the per-particle bytes.
+#include "nau_internal.cuh"
+
+namespace nau {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+inline int blocks_for(long n, int b = kBlock) { return (int)((n + b - 1) / b); }
+
+__global__ void k_boundary_shift(DomainDev d, long n, double* pos, uint8_t* active, DevErr* err) {
+    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n || !active[k]) return;
+    unsigned long long warn = 0;
+    for (int a = 0; a < d.dim; ++a) {
+        double* xp = pos + a * n + k;
+        double x = *xp;
+        const double lo = d.lo[a], hi = d.hi[a];
+        if (d.kind[a] == NAU_PERIODIC) {
+            if (x < lo || x >= hi) {
+                double w = fmod(x - lo, d.ext[a]);
+                if (w < 0.0) w += d.ext[a];
+                x = lo + w;
+                if (x >= hi) x = lo;  // seam guard
+                *xp = x;
+            }
+        } else if (d.kind[a] == NAU_SYMMETRIC) {
+            if (x < lo || x > hi) ++warn;
+        } else if (x < lo || x > hi) {
+            active[k] = 0;
+            break;
+        }
+    }
+    if (warn) atomicAdd(&err->warnings, warn);
+}
+
+__global__ void k_hash(DomainDev d, long n, const double* pos, const uint8_t* active,
+                       const int* orig, int* key, int* count, DevErr* err) {
+    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int flat = d.ncells;
+    if (active[k]) {
+        flat = 0;
+        for (int a = d.dim - 1; a >= 0; --a) {
+            double x = pos[a * n + k];
+            if (d.kind[a] == NAU_CUTOFF && (x < d.lo[a] || x > d.hi[a]))
+                latch_error(err, 4, kMsgOutsideCutoff, orig[k]);
+            flat = flat * d.cells[a] + cell_index(d, a, x);
+        }
+    }
+    key[k] = flat;
+    atomicAdd(&count[flat], 1);
+}
+
+// ---- exclusive scan of int32 (three-phase: tile scan, tile-sum scan, add) ----
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int* total) {
+    __shared__ int warp_sums[kScanThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int s = lane < kScanThreads / 32 ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < kScanThreads / 32) warp_sums[lane] = s;
+    }
+    __syncthreads();
+    int before = wid > 0 ? warp_sums[wid - 1] : 0;
+    *total = warp_sums[kScanThreads / 32 - 1];
+    __syncthreads();
+    return before + x - v;
+}
+
+__global__ void k_scan_tiles(const int* in, int* out, long n, int* tile_sums) {
+    long base = (long)blockIdx.x * kScanTile + (long)threadIdx.x * kScanItems;
+    int v[kScanItems];
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        v[i] = base + i < n ? in[base + i] : 0;
+        s += v[i];
+    }
+    int total;
+    int run = block_exclusive_scan(s, &total);
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        if (base + i < n) out[base + i] = run;
+        run += v[i];
+    }
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+// Single block: exclusive scan of the tile sums in place (any count).
+__global__ void k_scan_sums(int* sums, int m) {
+    int carry = 0;
+    for (int base = 0; base < m; base += kScanThreads) {
+        int i = base + threadIdx.x;
+        int v = i < m ? sums[i] : 0;
+        int total;
+        int ex = block_exclusive_scan(v, &total);
+        if (i < m) sums[i] = carry + ex;
+        carry += total;
+        __syncthreads();
+    }
+}
+
+__global__ void k_scan_add(int* out, long n, const int* tile_sums) {
+    long base = (long)blockIdx.x * kScanTile;
+    int add = tile_sums[blockIdx.x];
+    for (int i = threadIdx.x; i < kScanTile; i += kScanThreads)
+        if (base + i < n) out[base + i] += add;
+}
+
+__global__ void k_scatter(long n, const int* key, const int* orig, const int* start, int* cursor,
+                          int* perm_tmp, int* okey) {
+    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int c = key[k];
+    int slot = start[c] + atomicAdd(&cursor[c], 1);
+    perm_tmp[slot] = (int)k;
+    okey[slot] = orig[k];
+}
+
+// Rank each slot inside its cell by original index (distinct keys, so the
+// ranks form a permutation of the cell's slots). The inactive tail bin keeps
+// scatter order: inactive particles take part in no sum.
+__global__ void k_rank(long n, int ncells, const int* key, const int* start, const int* count,
+                       const int* perm_tmp, const int* okey, int* perm) {
+    long s = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    int k = perm_tmp[s];
+    int c = key[k];
+    if (c == ncells) {
+        perm[s] = k;
+        return;
+    }
+    int st = start[c], cnt = count[c];
+    int my = okey[s];
+    int rank = 0;
+    for (int t = st; t < st + cnt; ++t) rank += okey[t] < my;
+    perm[st + rank] = k;
+}
+
+struct ReorderTable {
+    int nf;
+    int comps[kMaxFields];
+    const double* src[kMaxFields];
+    double* dst[kMaxFields];
+};
+
+__global__ void k_reorder(long n, const int* perm, const int* orig, const int* key,
+                          const uint8_t* active, int* orig_s, int* key_s, uint8_t* active_s,
+                          ReorderTable t) {
+    long s = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    int k = perm[s];
+    orig_s[s] = orig[k];
+    key_s[s] = key[k];
+    active_s[s] = active[k];
+    for (int f = 0; f < t.nf; ++f) {
+        const double* src = t.src[f];
+        double* dst = t.dst[f];
+        for (int c = 0; c < t.comps[f]; ++c) dst[c * n + s] = src[c * n + k];
+    }
+}
+
+template <int DIM>
+__global__ void k_neighbor_counts(Geo g, double radius, int* out) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= *g.nact) return;
+    double xi[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < DIM; ++a) xi[a] = g.x[a * g.n + k];
+    int cnt = 0;
+    for_each_candidate<DIM>(g, k, xi, [&](int, const double* rel, int) {
+        if (norm_rel<DIM>(rel) <= radius) ++cnt;
+    });
+    out[g.orig[k]] = cnt;
+}
+
+__global__ void k_unsort(long n, int comps, const int* orig, const double* src, double* dst) {
+    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    long o = orig[k];
+    for (int c = 0; c < comps; ++c) dst[c * n + o] = src[c * n + k];
+}
+
+__global__ void k_sort_in(long n, int comps, const int* orig, const double* src, double* dst) {
+    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    long o = orig[k];
+    for (int c = 0; c < comps; ++c) dst[c * n + k] = src[c * n + o];
+}
+
+void scan_exclusive(nau_ctx* c, const int* in, int* out, long n) {
+    int tiles = (int)((n + kScanTile - 1) / kScanTile);
+    k_scan_tiles<<<tiles, kScanThreads, 0, c->stream>>>(in, out, n, c->d_scan_tmp);
+    k_scan_sums<<<1, kScanThreads, 0, c->stream>>>(c->d_scan_tmp, tiles);
+    k_scan_add<<<tiles, kScanThreads, 0, c->stream>>>(out, n, c->d_scan_tmp);
+    c->launches += 3;
+}
+
+}  // namespace
+
+void launch_boundary_shift(nau_ctx* c) {
+    if (c->n == 0) return;
+    k_boundary_shift<<<blocks_for(c->n), kBlock, 0, c->stream>>>(c->dom, c->n, c->fields[0].d,
+                                                                 c->d_active, c->d_err);
+    c->launches++;
+}
+
+void launch_build_cells(nau_ctx* c) {
+    const long n = c->n;
+    const int nc = c->dom.ncells;
+    cudaMemsetAsync(c->d_cell_count, 0, sizeof(int) * (nc + 1), c->stream);
+    cudaMemsetAsync(c->d_cursor, 0, sizeof(int) * (nc + 1), c->stream);
+    if (n > 0) {
+        k_hash<<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_active,
+                                                        c->d_orig, c->d_key, c->d_cell_count,
+                                                        c->d_err);
+        c->launches++;
+    }
+    // cell_start[ncells] (start of the inactive tail bin) = number of active particles.
+    scan_exclusive(c, c->d_cell_count, c->d_cell_start, nc + 1);
+    if (n == 0) return;
+    k_scatter<<<blocks_for(n), kBlock, 0, c->stream>>>(n, c->d_key, c->d_orig, c->d_cell_start,
+                                                       c->d_cursor, c->d_perm_tmp, c->d_okey);
+    k_rank<<<blocks_for(n), kBlock, 0, c->stream>>>(n, nc, c->d_key, c->d_cell_start,
+                                                    c->d_cell_count, c->d_perm_tmp, c->d_okey,
+                                                    c->d_perm);
+    ReorderTable t{};
+    for (size_t f = 0; f < c->fields.size(); ++f) {
+        FieldBuf& fb = c->fields[f];
+        if (!fb.live) continue;
+        t.comps[t.nf] = fb.comps();
+        t.src[t.nf] = fb.d;
+        t.dst[t.nf] = fb.alt;
+        ++t.nf;
+    }
+    k_reorder<<<blocks_for(n), kBlock, 0, c->stream>>>(n, c->d_perm, c->d_orig, c->d_key,
+                                                       c->d_active, c->d_orig_s, c->d_key_s,
+                                                       c->d_active_s, t);
+    c->launches += 3;
+    std::swap(c->d_orig, c->d_orig_s);
+    std::swap(c->d_key, c->d_key_s);
+    std::swap(c->d_active, c->d_active_s);
+    for (auto& fb : c->fields)
+        if (fb.live) std::swap(fb.d, fb.alt);
+}
+
+void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig) {
+    cudaMemsetAsync(d_out_orig, 0, sizeof(int) * c->n, c->stream);
+    if (c->n == 0) return;
+    Geo g = make_geo(c);
+    int b = blocks_for(c->n, 128);
+    switch (c->dom.dim) {
+        case 1: k_neighbor_counts<1><<<b, 128, 0, c->stream>>>(g, radius, d_out_orig); break;
+        case 2: k_neighbor_counts<2><<<b, 128, 0, c->stream>>>(g, radius, d_out_orig); break;
+        default: k_neighbor_counts<3><<<b, 128, 0, c->stream>>>(g, radius, d_out_orig); break;
+    }
+    c->launches++;
+}
+
+void launch_unsort(nau_ctx* c, const double* d_src, double* d_dst, int comps) {
+    if (c->n == 0) return;
+    k_unsort<<<blocks_for(c->n), kBlock, 0, c->stream>>>(c->n, comps, c->d_orig, d_src, d_dst);
+    c->launches++;
+}
+
+void launch_sort_in(nau_ctx* c, const double* d_src_orig, double* d_dst, int comps) {
+    if (c->n == 0) return;
+    k_sort_in<<<blocks_for(c->n), kBlock, 0, c->stream>>>(c->n, comps, c->d_orig, d_src_orig,
+                                                          d_dst);
+    c->launches++;
+}
+
+}  // namespace nau

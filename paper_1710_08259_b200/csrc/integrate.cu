@@ -1,0 +1,326 @@
+// integrate.cu — elementwise update kernels and the fused weakly-compressible
+// SPH deck of BASELINE cfg0/cfg2.
+//
+//   k_euler       ≙ EulerNode::evaluate (src/sfl/ast.cpp:180-191), active particles only
+//                   (inactive keep their value, src/case.cpp:36-40)
+//   k_symplectic  ≙ v = euler(v, vdot*mask, dt); r = euler(r, v, dt); apply_boundary_shift
+//                   (deck order dam_break_2d.yaml:37-38; case.cpp:59-62; particle_system.cpp:56-90)
+//   k_wcsph_*     the BASELINE dam-break equations as two neighbour passes (see
+//                 nauticle_gpu.h nau_wcsph_step) with per-operator accumulators
+//                 combined in the RHS expression's evaluation order (ast.cpp:71-94).
+// Compiled with -fmad=false like interact.cu.
+#include <cmath>
+#include <cstring>
+
+#include "nau_internal.cuh"
+
+namespace nau {
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kThreads = 128;
+inline int blocks_for(long n, int b = kBlock) { return (int)((n + b - 1) / b); }
+
+__global__ void k_euler(long n, int comps, const uint8_t* active, const int* orig, const double* x,
+                        const double* xdot, double dt, double* out, DevErr* err) {
+    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const bool act = active[k];
+    for (int c = 0; c < comps; ++c) {
+        double v = x[c * n + k];
+        if (act) {
+            v = v + dt * xdot[c * n + k];
+            if (!isfinite(v)) latch_error(err, 2, kMsgNan, orig[k]);
+        }
+        out[c * n + k] = v;
+    }
+}
+
+// One thread per particle: the two euler equations then the boundary shift of r.
+__global__ void k_symplectic(DomainDev d, long n, double* pos, double* v, const double* vdot,
+                             const double* mask, double dt, uint8_t* active, const int* orig,
+                             DevErr* err) {
+    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n || !active[k]) return;
+    const double mk = mask ? mask[k] : 1.0;
+    double vn[3];
+    bool bad = false;
+    for (int a = 0; a < d.dim; ++a) {
+        // euler(v, vdot*mask, dt): vdot*mask is mask * vdot (scalar broadcast, tensor.cpp:55-57)
+        double xd = mask ? mk * vdot[a * n + k] : vdot[a * n + k];
+        vn[a] = v[a * n + k] + dt * xd;
+        bad |= !isfinite(vn[a]);
+        v[a * n + k] = vn[a];
+    }
+    if (bad) latch_error(err, 2, kMsgNan, orig[k]);
+    bad = false;
+    unsigned long long warn = 0;
+    for (int a = 0; a < d.dim; ++a) {
+        double x = pos[a * n + k] + dt * vn[a];
+        bad |= !isfinite(x);
+        pos[a * n + k] = x;
+    }
+    if (bad) latch_error(err, 2, kMsgNan, orig[k]);
+    // apply_boundary_shift (particle_system.cpp:56-90)
+    for (int a = 0; a < d.dim; ++a) {
+        double x = pos[a * n + k];
+        const double lo = d.lo[a], hi = d.hi[a];
+        if (d.kind[a] == NAU_PERIODIC) {
+            if (x < lo || x >= hi) {
+                double w = fmod(x - lo, d.ext[a]);
+                if (w < 0.0) w += d.ext[a];
+                x = lo + w;
+                if (x >= hi) x = lo;
+                pos[a * n + k] = x;
+            }
+        } else if (d.kind[a] == NAU_SYMMETRIC) {
+            if (x < lo || x > hi) ++warn;
+        } else if (x < lo || x > hi) {
+            active[k] = 0;
+            break;
+        }
+    }
+    if (warn) atomicAdd(&err->warnings, warn);
+}
+
+struct WcsphArgs {
+    Geo g;
+    double mass, radius, rho0, B, gamma, visc, g_acc[3];
+    int kdim;
+    double* rho;
+    double* p;
+    const double* v;
+    double* vdot;
+    DevErr* err;
+};
+
+// Pass 1: rho = sph_S(one, m, one, K, R) (interactions.cpp:40-58 with A = rho = 1),
+//         p = B*((rho/rho0)^gamma - 1).
+template <int DIM, int KF>
+__global__ void __launch_bounds__(kThreads) k_wcsph_density(const __grid_constant__ WcsphArgs a) {
+    const Geo& g = a.g;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= *g.nact) return;
+    const long n = g.n;
+    double xi[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) xi[d] = g.x[d * n + k];
+    const double radius = a.radius;
+    const double h = 0.5 * radius;
+    const double alpha = kernel_alpha<KF>(a.kdim, h);
+    const double s_unit = a.mass / 1.0;  // m_j / rho_j with the uniform operand rho = 1
+    double acc = 0.0;
+    for_each_candidate<DIM>(g, k, xi, [&](int, const double* rel, int) {
+        const double dist = norm_rel<DIM>(rel);
+        if (dist > radius) return;
+        const double w = kernel_value<KF>(alpha, h, dist);
+        if (w == 0.0) return;
+        acc = acc + 1.0 * (s_unit * w);
+    });
+    const double p = a.B * (pow(acc / a.rho0, a.gamma) - 1.0);
+    if (!isfinite(acc) || !isfinite(p)) latch_error(a.err, 2, kMsgNan, g.orig[k]);
+    a.rho[k] = acc;
+    a.p[k] = p;
+}
+
+// Pass 2: vdot = -1/rho*sph_G11(p,m,rho,K,R) + visc*sph_A(v,m,rho,K,R) + g, one
+// neighbour walk with the two operators' accumulators kept apart.
+template <int DIM, int KF>
+__global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_constant__ WcsphArgs a) {
+    const Geo& g = a.g;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= *g.nact) return;
+    const long n = g.n;
+    double xi[3] = {0.0, 0.0, 0.0}, v_i[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+        xi[d] = g.x[d * n + k];
+        v_i[d] = a.v[d * n + k];
+    }
+    const double radius = a.radius;
+    const double h = 0.5 * radius;
+    const double alpha = kernel_alpha<KF>(a.kdim, h);
+    const double m = a.mass;
+    const double rho_i = a.rho[k];
+    const double p_i = a.p[k];
+    const int my_orig = g.orig[k];
+    if (rho_i == 0.0) {
+        latch_error(a.err, 1, kMsgZeroDensity, my_orig);
+        return;
+    }
+    const double pr_i = p_i / (rho_i * rho_i);
+    double G[3] = {0.0, 0.0, 0.0}, A[3] = {0.0, 0.0, 0.0};
+    for_each_candidate<DIM>(g, k, xi, [&](int j, const double* rel, int mask) {
+        const double dist = norm_rel<DIM>(rel);
+        if (dist > radius) return;
+        if (dist <= 0.0) {  // G11 skips silently; sph_A warns (interactions.cpp:32-38)
+            if (g.orig[j] != my_orig && mask == 0) atomicAdd(&a.err->warnings, 1ull);
+            return;
+        }
+        const double sc = kernel_grad_scale<KF>(alpha, h, dist);
+        const double rho_j = a.rho[j];
+        if (rho_j == 0.0) {
+            latch_error(a.err, 1, kMsgZeroDensity, g.orig[j]);
+            return;
+        }
+        const double s = m * (pr_i + a.p[j] / (rho_j * rho_j));
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) G[d] = G[d] + (rel[d] * sc) * s;
+        double ap = (mirror_comp(a.v[j], 0, DIM, 1, mask, DIM) - v_i[0]) * rel[0];
+#pragma unroll
+        for (int d = 1; d < DIM; ++d)
+            ap = ap + (mirror_comp(a.v[d * n + j], d, DIM, 1, mask, DIM) - v_i[d]) * rel[d];
+        if (ap >= 0.0) return;
+        const double pi_ij = ap / (rho_i * dist * dist);
+        const double sa = m * pi_ij;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) A[d] = A[d] + (rel[d] * sc) * sa;
+    });
+    const double s1 = -1.0 / rho_i;
+    bool bad = false;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+        const double gd = rho_i * G[d];
+        const double r = (s1 * gd + a.visc * A[d]) + a.g_acc[d];
+        bad |= !isfinite(r);
+        a.vdot[d * n + k] = r;
+    }
+    if (bad) latch_error(a.err, 2, kMsgNan, my_orig);
+}
+
+// ---- reductions (fmax/fmin/fsum/fmean), ast.cpp:237-274 ----
+constexpr int kRedThreads = 256;
+constexpr int kRedBlocks = 296;  // 2 x 148 SMs
+
+__global__ void k_reduce_partial(long n, int comps, int kind, const uint8_t* active,
+                                 const double* f, double* part, unsigned long long* cnt) {
+    __shared__ double sh[kRedThreads][9];
+    double acc[9];
+    for (int c = 0; c < 9; ++c) acc[c] = kind == 0 ? -INFINITY : (kind == 1 ? INFINITY : 0.0);
+    unsigned long long my = 0;
+    for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+        if (!active[k]) continue;
+        ++my;
+        if (kind >= 2) {
+            for (int c = 0; c < comps; ++c) acc[c] += f[c * n + k];
+        } else {
+            double s;
+            if (comps == 1) {
+                s = f[k];
+            } else {
+                s = f[k] * f[k];
+                for (int c = 1; c < comps; ++c) s = s + f[c * n + k] * f[c * n + k];
+                s = sqrt(s);
+            }
+            acc[0] = kind == 0 ? fmax(acc[0], s) : fmin(acc[0], s);
+        }
+    }
+    for (int c = 0; c < 9; ++c) sh[threadIdx.x][c] = acc[c];
+    atomicAdd(cnt, my);
+    __syncthreads();
+    for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            for (int c = 0; c < 9; ++c) {
+                double o = sh[threadIdx.x + s][c];
+                double& t = sh[threadIdx.x][c];
+                t = kind == 0 ? fmax(t, o) : (kind == 1 ? fmin(t, o) : t + o);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int c = 0; c < 9; ++c) part[blockIdx.x * 9 + c] = sh[0][c];
+}
+
+template <int DIM>
+void wcsph_launch(nau_ctx* c, const WcsphArgs& a, int kf) {
+    const int blocks = (int)((c->n + kThreads - 1) / kThreads);
+    prof_begin(c, 200);
+    if (kf == NAU_K_CUBIC) {
+        k_wcsph_density<DIM, NAU_K_CUBIC><<<blocks, kThreads, 0, c->stream>>>(a);
+    } else {
+        k_wcsph_density<DIM, NAU_K_WENDLAND><<<blocks, kThreads, 0, c->stream>>>(a);
+    }
+    prof_end(c, 200);
+    prof_begin(c, 201);
+    if (kf == NAU_K_CUBIC) {
+        k_wcsph_momentum<DIM, NAU_K_CUBIC><<<blocks, kThreads, 0, c->stream>>>(a);
+    } else {
+        k_wcsph_momentum<DIM, NAU_K_WENDLAND><<<blocks, kThreads, 0, c->stream>>>(a);
+    }
+    prof_end(c, 201);
+    c->launches += 2;
+}
+
+}  // namespace
+
+void launch_euler(nau_ctx* c, const double* x, const double* xdot, double dt, double* out,
+                  int comps) {
+    if (c->n == 0) return;
+    k_euler<<<blocks_for(c->n), kBlock, 0, c->stream>>>(c->n, comps, c->d_active, c->d_orig, x,
+                                                         xdot, dt, out, c->d_err);
+    c->launches++;
+}
+
+void launch_symplectic(nau_ctx* c, double* v, const double* vdot, const double* mask, double dt) {
+    if (c->n == 0) return;
+    prof_begin(c, 301);
+    k_symplectic<<<blocks_for(c->n), kBlock, 0, c->stream>>>(c->dom, c->n, c->fields[0].d, v, vdot,
+                                                              mask, dt, c->d_active, c->d_orig,
+                                                              c->d_err);
+    prof_end(c, 301);
+    c->launches++;
+}
+
+void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p) {
+    if (c->n == 0) return;
+    WcsphArgs a;
+    a.g = make_geo(c);
+    a.mass = p->mass;
+    a.radius = p->radius;
+    a.rho0 = p->rho0;
+    a.B = p->B;
+    a.gamma = p->gamma;
+    a.visc = p->visc;
+    for (int d = 0; d < 3; ++d) a.g_acc[d] = p->g[d];
+    a.kdim = p->kernel_dim;
+    a.rho = c->fields[p->f_rho].d;
+    a.p = c->fields[p->f_p].d;
+    a.v = c->fields[p->f_v].d;
+    a.vdot = c->fields[p->f_vdot].d;
+    a.err = c->d_err;
+    switch (c->dom.dim) {
+        case 1: wcsph_launch<1>(c, a, p->kernel_family); break;
+        case 2: wcsph_launch<2>(c, a, p->kernel_family); break;
+        default: wcsph_launch<3>(c, a, p->kernel_family); break;
+    }
+    const double* mask = p->f_mask >= 0 ? c->fields[p->f_mask].d : nullptr;
+    launch_symplectic(c, c->fields[p->f_v].d, c->fields[p->f_vdot].d, mask, p->dt);
+}
+
+void launch_reduce(nau_ctx* c, int kind, const double* f, int comps, double* h_out) {
+    double* part = c->d_red;
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(c->d_red + kRedBlocks * 9);
+    cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), c->stream);
+    k_reduce_partial<<<kRedBlocks, kRedThreads, 0, c->stream>>>(c->n, comps, kind, c->d_active, f,
+                                                                 part, cnt);
+    c->launches++;
+    std::vector<double> h(kRedBlocks * 9 + 1);
+    cudaMemcpyAsync(h.data(), part, sizeof(double) * (kRedBlocks * 9 + 1), cudaMemcpyDeviceToHost,
+                    c->stream);
+    cudaStreamSynchronize(c->stream);
+    unsigned long long count = 0;
+    std::memcpy(&count, &h[kRedBlocks * 9], sizeof(count));
+    const int oc = kind >= 2 ? comps : 1;
+    for (int q = 0; q < oc; ++q) {
+        double acc = kind == 0 ? -INFINITY : (kind == 1 ? INFINITY : 0.0);
+        for (int b = 0; b < kRedBlocks; ++b) {
+            double v = h[b * 9 + q];
+            acc = kind == 0 ? std::fmax(acc, v) : (kind == 1 ? std::fmin(acc, v) : acc + v);
+        }
+        if (kind == 3) acc = acc / (double)count;
+        h_out[q] = acc;
+    }
+}
+
+}  // namespace nau

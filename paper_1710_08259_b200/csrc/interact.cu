@@ -1,0 +1,460 @@
+// interact.cu — the interaction-operator evaluators of kOps[] (src/interactions.cpp:259-269)
+// as whole-field sm_100a kernels.
+//
+// One thread owns one particle slot k (cell order) and walks the 3^d stencil
+// in the reference's candidate order (particle_system.hpp:59-138), so every
+// accumulator sums in the same order as interact() (interactions.hpp:29-36).
+// Consecutive threads are consecutive particles of the same / adjacent cells,
+// so a warp's candidate loads hit the same few cache lines (L1 broadcast).
+// This TU is compiled with -fmad=false: with IEEE div/sqrt the results are
+// bitwise identical to the reference wherever no libm transcendental (pow/log)
+// enters (Hertz DEM, gravity, Tait EOS are tolerance-checked).
+#include <cmath>
+#include <cstring>
+
+#include "nau_internal.cuh"
+
+namespace nau {
+
+namespace {
+
+constexpr int kThreads = 128;
+
+struct SphArgs {
+    Geo g;
+    Opd A, m, rho, R;
+    double* out;
+    int arows, acols;
+    int kdim;
+    DevErr* err;
+};
+
+template <int DIM, int OP, int KF, int AC>
+__global__ void __launch_bounds__(kThreads) k_sph(const __grid_constant__ SphArgs a) {
+    const Geo& g = a.g;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= *g.nact) return;
+    const long n = g.n;
+    double xi[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) xi[d] = g.x[d * n + k];
+    // sph_context (interactions.cpp:22-27)
+    const double radius = a.R.at(0, k, n);
+    if (!(radius > 0.0)) {
+        latch_error(a.err, 1, kMsgRadius, g.orig[k]);
+        return;
+    }
+    const double h = 0.5 * radius;
+    const double alpha = kernel_alpha<KF>(a.kdim, h);
+    const int ac = AC == 1 ? 1 : a.arows * a.acols;
+    double a_i[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) a_i[c] = (c < ac) ? a.A.at(c, k, n) : 0.0;
+    double rho_i = 1.0;
+    if (OP == NAU_OP_SPH_G11 || OP == NAU_OP_SPH_A) {
+        rho_i = a.rho.at(0, k, n);
+        if (rho_i == 0.0) {
+            latch_error(a.err, 1, kMsgZeroDensity, g.orig[k]);
+            return;
+        }
+    }
+    double acc[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) acc[c] = 0.0;
+    const int my_orig = g.orig[k];
+
+    for_each_candidate<DIM>(g, k, xi, [&](int j, const double* rel, int mask) {
+        const double dist = norm_rel<DIM>(rel);
+        if (OP == NAU_OP_SPH_S) {  // interactions.cpp:40-58
+            if (dist > radius) return;
+            const double w = kernel_value<KF>(alpha, h, dist);
+            if (w == 0.0) return;
+            const double rho_j = a.rho.at(0, j, n);
+            if (rho_j == 0.0) {
+                latch_error(a.err, 1, kMsgZeroDensity, g.orig[j]);
+                return;
+            }
+            const double m_j = a.m.at(0, j, n);
+            const double s = m_j / rho_j * w;
+#pragma unroll
+            for (int c = 0; c < (AC == 1 ? 1 : 9); ++c)
+                if (c < ac)
+                    acc[c] = acc[c] + mirror_comp(a.A.at(c, j, n), c, a.arows, a.acols, mask, DIM) * s;
+        } else if (OP == NAU_OP_SPH_D00) {  // interactions.cpp:60-79
+            if (dist <= 0.0 || dist > radius) return;
+            const double rho_j = a.rho.at(0, j, n);
+            if (rho_j == 0.0) {
+                latch_error(a.err, 1, kMsgZeroDensity, g.orig[j]);
+                return;
+            }
+            const double m_j = a.m.at(0, j, n);
+            const double sc = kernel_grad_scale<KF>(alpha, h, dist);
+            double dt = (mirror_comp(a.A.at(0, j, n), 0, DIM, 1, mask, DIM) - a_i[0]) * (rel[0] * sc);
+#pragma unroll
+            for (int d = 1; d < DIM; ++d)
+                dt = dt + (mirror_comp(a.A.at(d, j, n), d, DIM, 1, mask, DIM) - a_i[d]) * (rel[d] * sc);
+            acc[0] = acc[0] + dt * (m_j / rho_j);
+        } else if (OP == NAU_OP_SPH_G11) {  // interactions.cpp:81-102
+            if (dist <= 0.0 || dist > radius) return;
+            const double rho_j = a.rho.at(0, j, n);
+            if (rho_j == 0.0) {
+                latch_error(a.err, 1, kMsgZeroDensity, g.orig[j]);
+                return;
+            }
+            const double a_j = a.A.at(0, j, n);
+            const double m_j = a.m.at(0, j, n);
+            const double sc = kernel_grad_scale<KF>(alpha, h, dist);
+            const double s = m_j * (a_i[0] / (rho_i * rho_i) + a_j / (rho_j * rho_j));
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) acc[d] = acc[d] + (rel[d] * sc) * s;
+        } else if (OP == NAU_OP_SPH_L0) {  // interactions.cpp:104-126
+            if (dist > radius) return;
+            if (dist <= 0.0) {  // warn_coincident (interactions.cpp:32-38)
+                if (g.orig[j] != my_orig && mask == 0) atomicAdd(&a.err->warnings, 1ull);
+                return;
+            }
+            const double rho_j = a.rho.at(0, j, n);
+            if (rho_j == 0.0) {
+                latch_error(a.err, 1, kMsgZeroDensity, g.orig[j]);
+                return;
+            }
+            const double a_j = a.A.at(0, j, n);
+            const double m_j = a.m.at(0, j, n);
+            const double sc = kernel_grad_scale<KF>(alpha, h, dist);
+            double rg = rel[0] * (rel[0] * sc);
+#pragma unroll
+            for (int d = 1; d < DIM; ++d) rg = rg + rel[d] * (rel[d] * sc);
+            acc[0] = acc[0] + 2.0 * (a_j - a_i[0]) * rg / (dist * dist) * m_j / rho_j;
+        } else {  // NAU_OP_SPH_A, interactions.cpp:128-150
+            if (dist > radius) return;
+            if (dist <= 0.0) {
+                if (g.orig[j] != my_orig && mask == 0) atomicAdd(&a.err->warnings, 1ull);
+                return;
+            }
+            double ap = (mirror_comp(a.A.at(0, j, n), 0, DIM, 1, mask, DIM) - a_i[0]) * rel[0];
+#pragma unroll
+            for (int d = 1; d < DIM; ++d)
+                ap = ap + (mirror_comp(a.A.at(d, j, n), d, DIM, 1, mask, DIM) - a_i[d]) * rel[d];
+            if (ap >= 0.0) return;
+            const double m_j = a.m.at(0, j, n);
+            const double pi_ij = ap / (rho_i * dist * dist);
+            const double sc = kernel_grad_scale<KF>(alpha, h, dist);
+            const double s = m_j * pi_ij;
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) acc[d] = acc[d] + (rel[d] * sc) * s;
+        }
+    });
+
+    int oc = 1;
+    if (OP == NAU_OP_SPH_S) oc = ac;
+    if (OP == NAU_OP_SPH_G11 || OP == NAU_OP_SPH_A) oc = DIM;
+    if (OP == NAU_OP_SPH_G11) {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) acc[d] = rho_i * acc[d];
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+        if (c < oc) {
+            if (!isfinite(acc[c])) latch_error(a.err, 2, kMsgNan, my_orig);
+            a.out[c * n + k] = acc[c];
+        }
+    }
+}
+
+// ---- DEM contact sums: dem_sum (interactions.cpp:152-193) ----
+struct DemArgs {
+    Geo g;
+    Opd v, R, P, Q, m, cf, Rs;  // P = E (Hertz) | kn (LSD); Q = nu (Hertz) | en (LSD)
+    double zeta_uniform;        // LSD damping ratio from a uniform en (host libm), else NaN
+    double* out;
+    DevErr* err;
+};
+
+template <int DIM, int OP>
+__global__ void __launch_bounds__(kThreads) k_dem(const __grid_constant__ DemArgs a) {
+    const Geo& g = a.g;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= *g.nact) return;
+    const long n = g.n;
+    constexpr bool kImagesOnly = OP == NAU_OP_DEM_BOUNDARY;
+    constexpr bool kLsd = OP == NAU_OP_DEM_LSD;
+    double xi[3] = {0.0, 0.0, 0.0}, v_i[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+        xi[d] = g.x[d * n + k];
+        v_i[d] = a.v.at(d, k, n);
+    }
+    const double radius = a.Rs.at(0, k, n);
+    const double Ri = a.R.at(0, k, n), Pi = a.P.at(0, k, n), Qi = a.Q.at(0, k, n);
+    const double mi = a.m.at(0, k, n), fr = a.cf.at(0, k, n);
+    double zeta = 0.0;
+    if (kLsd) {
+        if (a.zeta_uniform == a.zeta_uniform) {
+            zeta = a.zeta_uniform;
+        } else {
+            double le = log(Qi);
+            zeta = -le / sqrt(kPi * kPi + le * le);
+        }
+    }
+    const int my_orig = g.orig[k];
+    double acc[3] = {0.0, 0.0, 0.0};
+    for_each_candidate<DIM>(g, k, xi, [&](int j, const double* rel, int mask) {
+        const double dist = norm_rel<DIM>(rel);
+        if (dist > radius) return;
+        if (kImagesOnly && mask == 0) return;
+        if (dist <= 0.0) {
+            if (!kLsd && g.orig[j] != my_orig && mask == 0) atomicAdd(&a.err->warnings, 1ull);
+            return;
+        }
+        const double Rj = a.R.at(0, j, n), Pj = a.P.at(0, j, n), Qj = a.Q.at(0, j, n);
+        const double mj = a.m.at(0, j, n);
+        if (Rj + Ri - dist <= 0.0) return;
+        double v_j[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) v_j[d] = mirror_comp(a.v.at(d, j, n), d, DIM, 1, mask, DIM);
+        // hertz_contact_force (interactions.cpp:288-316) / linear spring-dashpot
+        const double overlap = Ri + Rj - dist;
+        double n_ji[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) n_ji[d] = rel[d] / dist;
+        double dd = (v_j[0] - v_i[0]) * n_ji[0];
+#pragma unroll
+        for (int d = 1; d < DIM; ++d) dd = dd + (v_j[d] - v_i[d]) * n_ji[d];
+        const double overlap_rate = -dd;
+        double normal;
+        if (kLsd) {
+            const double kn = Pi;
+            const double m_eff = mi * mj / (mi + mj);
+            const double c_n = 2.0 * zeta * sqrt(m_eff * kn);
+            normal = kn * overlap + c_n * overlap_rate;
+        } else {
+            if (Pi <= 0.0 || Pj <= 0.0 || Ri <= 0.0 || Rj <= 0.0) {
+                latch_error(a.err, 1, kMsgDemParams, my_orig);
+                return;
+            }
+            const double r_eff = Ri * Rj / (Ri + Rj);
+            const double m_eff = mi * mj / (mi + mj);
+            const double e_eff = Pi * Pj / (Pj * (1.0 - Qi * Qi) + Pi * (1.0 - Qj * Qj));
+            const double k_hz = 4.0 / 3.0 * sqrt(r_eff) * e_eff;
+            const double c_hz = sqrt(m_eff * k_hz) / 8.0 * 1.0;
+            normal = k_hz * pow(overlap, 1.5) + c_hz * pow(overlap, 0.25) * overlap_rate;
+        }
+        double f[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) f[d] = -(n_ji[d] * normal);
+        if (fr != 0.0) {
+            double v_ij[3], v_t[3];
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) v_ij[d] = v_i[d] - v_j[d];
+            double dn = v_ij[0] * n_ji[0];
+#pragma unroll
+            for (int d = 1; d < DIM; ++d) dn = dn + v_ij[d] * n_ji[d];
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) v_t[d] = -v_ij[d] + n_ji[d] * dn;
+            const double vt_norm = norm_rel<DIM>(v_t);
+            if (vt_norm > 1e-12) {
+                const double s = fr * fabs(normal) / vt_norm;
+#pragma unroll
+                for (int d = 0; d < DIM; ++d) f[d] = f[d] + v_t[d] * s;
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) acc[d] = acc[d] + f[d];
+    });
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+        double r = kImagesOnly ? acc[d] : acc[d] / mi;
+        if (!isfinite(r)) latch_error(a.err, 2, kMsgNan, my_orig);
+        a.out[d * n + k] = r;
+    }
+}
+
+// ---- all-pairs softened gravity: eval_gravity (interactions.cpp:195-214) ----
+// j-tiles of positions/masses staged in shared memory; each thread sums its
+// body's acceleration over j in storage order (the reference order when no
+// cell build has permuted the bodies).
+constexpr int kGravTile = 256;
+
+struct GravArgs {
+    long n;
+    const double* x;
+    const uint8_t* active;
+    const int* orig;
+    Opd m, G, eps;
+    int has_eps;
+    double* out;
+    DevErr* err;
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(kGravTile) k_gravity(const __grid_constant__ GravArgs a) {
+    __shared__ double sx[3][kGravTile];
+    __shared__ double sm[kGravTile];
+    __shared__ unsigned char sa[kGravTile];
+    const long n = a.n;
+    const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    const bool mine = k < n && a.active[k];
+    double xi[3] = {0.0, 0.0, 0.0};
+    double G = 0.0, eps = 0.0;
+    if (mine) {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) xi[d] = a.x[d * n + k];
+        G = a.G.at(0, k, n);
+        eps = a.has_eps ? a.eps.at(0, k, n) : 0.0;
+    }
+    const double eps2 = eps * eps;
+    double acc[3] = {0.0, 0.0, 0.0};
+    bool coincident = false;
+    for (long base = 0; base < n; base += kGravTile) {
+        const long j = base + threadIdx.x;
+        if (j < n) {
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) sx[d][threadIdx.x] = a.x[d * n + j];
+            sm[threadIdx.x] = a.m.at(0, (int)j, n);
+            sa[threadIdx.x] = a.active[j];
+        } else {
+            sa[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        if (mine) {
+            const int lim = (int)min((long)kGravTile, n - base);
+            for (int t = 0; t < lim; ++t) {
+                if (base + t == k || !sa[t]) continue;
+                double rel[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+                for (int d = 0; d < DIM; ++d) rel[d] = sx[d][t] - xi[d];
+                double r2 = rel[0] * rel[0];
+#pragma unroll
+                for (int d = 1; d < DIM; ++d) r2 = r2 + rel[d] * rel[d];
+                r2 = r2 + eps2;
+                if (r2 == 0.0) {
+                    coincident = true;
+                    continue;
+                }
+                const double s = G * sm[t] / (r2 * sqrt(r2));
+#pragma unroll
+                for (int d = 0; d < DIM; ++d) acc[d] = acc[d] + rel[d] * s;
+            }
+        }
+        __syncthreads();
+    }
+    if (!mine) return;
+    if (coincident) latch_error(a.err, 1, kMsgCoincident, a.orig[k]);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+        if (!isfinite(acc[d])) latch_error(a.err, 2, kMsgNan, a.orig[k]);
+        a.out[d * n + k] = acc[d];
+    }
+}
+
+template <int DIM, int OP, int KF>
+void sph_launch(nau_ctx* c, const SphArgs& a, int ac) {
+    const int blocks = (int)((c->n + kThreads - 1) / kThreads);
+    if (OP == NAU_OP_SPH_S && ac > 1)
+        k_sph<DIM, OP, KF, 9><<<blocks, kThreads, 0, c->stream>>>(a);
+    else
+        k_sph<DIM, OP, KF, 1><<<blocks, kThreads, 0, c->stream>>>(a);
+}
+
+template <int DIM, int OP>
+void sph_launch_kf(nau_ctx* c, const SphArgs& a, int kf, int ac) {
+    if (kf == NAU_K_CUBIC)
+        sph_launch<DIM, OP, NAU_K_CUBIC>(c, a, ac);
+    else
+        sph_launch<DIM, OP, NAU_K_WENDLAND>(c, a, ac);
+}
+
+template <int DIM>
+void sph_dispatch(nau_ctx* c, int op, const SphArgs& a, int kf, int ac) {
+    switch (op) {
+        case NAU_OP_SPH_S: sph_launch_kf<DIM, NAU_OP_SPH_S>(c, a, kf, ac); break;
+        case NAU_OP_SPH_D00: sph_launch_kf<DIM, NAU_OP_SPH_D00>(c, a, kf, ac); break;
+        case NAU_OP_SPH_G11: sph_launch_kf<DIM, NAU_OP_SPH_G11>(c, a, kf, ac); break;
+        case NAU_OP_SPH_L0: sph_launch_kf<DIM, NAU_OP_SPH_L0>(c, a, kf, ac); break;
+        default: sph_launch_kf<DIM, NAU_OP_SPH_A>(c, a, kf, ac); break;
+    }
+}
+
+template <int DIM>
+void dem_dispatch(nau_ctx* c, int op, const DemArgs& a) {
+    const int blocks = (int)((c->n + kThreads - 1) / kThreads);
+    if (op == NAU_OP_DEM_LSD)
+        k_dem<DIM, NAU_OP_DEM_LSD><<<blocks, kThreads, 0, c->stream>>>(a);
+    else if (op == NAU_OP_DEM_BOUNDARY)
+        k_dem<DIM, NAU_OP_DEM_BOUNDARY><<<blocks, kThreads, 0, c->stream>>>(a);
+    else
+        k_dem<DIM, NAU_OP_DEM_HERTZ><<<blocks, kThreads, 0, c->stream>>>(a);
+}
+
+}  // namespace
+
+void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int nops, double* out,
+                     int out_rows, int out_cols, int a_rows, int a_cols) {
+    (void)out_rows;
+    (void)out_cols;
+    if (c->n == 0) return;
+    const int dim = c->dom.dim;
+    if (op <= NAU_OP_SPH_A) {
+        SphArgs a;
+        a.g = make_geo(c);
+        a.A = ops[0];
+        a.m = ops[1];
+        a.rho = ops[2];
+        a.R = ops[3];
+        a.out = out;
+        a.arows = a_rows;
+        a.acols = a_cols;
+        a.kdim = kdim;
+        a.err = c->d_err;
+        const int ac = a_rows * a_cols;
+        prof_begin(c, 100 + op);
+        if (dim == 1) sph_dispatch<1>(c, op, a, kf, ac);
+        else if (dim == 2) sph_dispatch<2>(c, op, a, kf, ac);
+        else sph_dispatch<3>(c, op, a, kf, ac);
+        prof_end(c, 100 + op);
+    } else if (op == NAU_OP_GRAVITY) {
+        GravArgs a;
+        a.n = c->n;
+        a.x = c->fields[0].d;
+        a.active = c->d_active;
+        a.orig = c->d_orig;
+        a.m = ops[0];
+        a.G = ops[1];
+        a.has_eps = nops > 2;
+        if (nops > 2) a.eps = ops[2];
+        else a.eps = ops[1];
+        a.out = out;
+        a.err = c->d_err;
+        const int blocks = (int)((c->n + kGravTile - 1) / kGravTile);
+        prof_begin(c, 100 + op);
+        if (dim == 1) k_gravity<1><<<blocks, kGravTile, 0, c->stream>>>(a);
+        else if (dim == 2) k_gravity<2><<<blocks, kGravTile, 0, c->stream>>>(a);
+        else k_gravity<3><<<blocks, kGravTile, 0, c->stream>>>(a);
+        prof_end(c, 100 + op);
+    } else {
+        DemArgs a;
+        a.g = make_geo(c);
+        a.v = ops[0];
+        a.R = ops[1];
+        a.P = ops[2];
+        a.Q = ops[3];
+        a.m = ops[4];
+        a.cf = ops[5];
+        a.Rs = ops[6];
+        a.zeta_uniform = __builtin_nan("");
+        if (op == NAU_OP_DEM_LSD && ops[3].p == nullptr) {
+            double le = std::log(ops[3].v[0]);
+            a.zeta_uniform = -le / std::sqrt(kPi * kPi + le * le);
+        }
+        a.out = out;
+        a.err = c->d_err;
+        prof_begin(c, 100 + op);
+        if (dim == 1) dem_dispatch<1>(c, op, a);
+        else if (dim == 2) dem_dispatch<2>(c, op, a);
+        else dem_dispatch<3>(c, op, a);
+        prof_end(c, 100 + op);
+    }
+    c->launches++;
+}
+
+}  // namespace nau

@@ -1,0 +1,358 @@
+// nau_internal.cuh — shared device/host definitions of libnau_b200.so.
+//
+// Data layout in HBM (one context = one GPU):
+//   * every field is an fp64 SoA array, component-major: f[c*n + k], c < rows*cols,
+//     k = CELL-ORDER slot (particles sorted by (flat cell, original index));
+//   * orig[k]   int32  original particle index of slot k;
+//   * key[k]    int32  flat cell of slot k (== ncells for inactive particles,
+//                      which therefore sort to the tail);
+//   * active[k] uint8  ParticleSystem::active_ (particle_system.hpp:145);
+//   * cell_start[c] / cell_count[c] int32 tables, c < ncells (+1 sentinel bin).
+// A rebuild (build_cells) permutes every array with one gather pass, so the
+// neighbour-sum kernels read each cell's particles as a contiguous range.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "nauticle_gpu.h"
+
+namespace nau {
+
+constexpr int kMaxFields = 64;
+constexpr double kPi = 3.14159265358979323846;
+
+struct DomainDev {
+    int dim;
+    int cells[3];
+    int ncells;
+    int kind[3];
+    double lo[3], hi[3], ext[3], cs[3];
+};
+
+// Latched device error word (surfaced by nau_sync).
+struct DevErr {
+    unsigned long long warnings;  // ≙ ParticleSystem::warnings_ (atomic counter)
+    long long first_bad;          // lowest original index of a runtime error
+    long long nan_first;          // lowest original index of a non-finite result
+    int code;                     // bit 1 runtime, bit 2 nan, bit 4 outside cutoff at build
+    int msg;                      // message id of the runtime error (see capi.cu)
+};
+
+enum ErrMsg {
+    kMsgNone = 0,
+    kMsgZeroDensity = 1,
+    kMsgRadius = 2,
+    kMsgOutsideCutoff = 3,
+    kMsgCoincident = 4,
+    kMsgDemParams = 5,
+    kMsgNan = 6,
+};
+
+// Operand as seen by a kernel: field pointer (cell order) or uniform value.
+struct Opd {
+    const double* p;
+    double v[9];
+    __device__ __forceinline__ double at(int c, int k, long n) const {
+        return p ? p[(long)c * n + k] : v[c];
+    }
+};
+
+// Geometry bundle handed to every neighbour kernel.
+struct Geo {
+    DomainDev dom;
+    long n;
+    const double* x;  // pos component 0..dim-1 (x + a*n)
+    const int* key;
+    const int* orig;
+    const uint8_t* active;
+    const int* cell_start;
+    const int* cell_count;
+    const int* nact;  // == cell_start[ncells]
+};
+
+struct FieldBuf {
+    int rows = 0, cols = 0;
+    double* d = nullptr;    // current storage (cell order)
+    double* alt = nullptr;  // reorder / two-phase twin, swapped with d
+    bool live = false;
+    int comps() const { return rows * cols; }
+};
+
+__device__ __forceinline__ void latch_error(DevErr* e, int code, int msg, long long particle) {
+    atomicOr(&e->code, code);
+    if (code & 1) {
+        atomicMin(&e->first_bad, particle);
+        atomicCAS(&e->msg, 0, msg);
+    } else if (code & 2) {
+        atomicMin(&e->nan_first, particle);
+    } else if (code & 4) {
+        atomicMin(&e->first_bad, particle);
+        atomicCAS(&e->msg, 0, msg);
+    }
+}
+
+// particle_system.cpp:20-31 — IEEE division then floor, periodic modulo / clamp.
+__device__ __forceinline__ int cell_index(const DomainDev& d, int a, double x) {
+    int n = d.cells[a];
+    int c = (int)floor((x - d.lo[a]) / d.cs[a]);
+    if (d.kind[a] == NAU_PERIODIC) {
+        c %= n;
+        if (c < 0) c += n;
+        return c;
+    }
+    return c < 0 ? 0 : (c >= n ? n - 1 : c);
+}
+
+// ---- smoothing kernels: src/kernel.cpp:37-69 (Wendland), cubic spline (new) ----
+// Operation order matches the reference's left-associative C++ expressions.
+template <int KF>
+__device__ __forceinline__ double kernel_alpha(int kdim, double h) {
+    if (KF == NAU_K_WENDLAND) {
+        if (kdim == 1) return 3.0 / (4.0 * h);
+        if (kdim == 2) return 7.0 / (4.0 * kPi * h * h);
+        return 21.0 / (16.0 * kPi * h * h * h);
+    } else {
+        if (kdim == 1) return 2.0 / (3.0 * h);
+        if (kdim == 2) return 10.0 / (7.0 * kPi * h * h);
+        return 1.0 / (kPi * h * h * h);
+    }
+}
+
+template <int KF>
+__device__ __forceinline__ double kernel_value(double alpha, double h, double dist) {
+    double q = dist / h;
+    if (q >= 2.0) return 0.0;
+    if (KF == NAU_K_WENDLAND) {
+        double t = 1.0 - 0.5 * q;
+        double t2 = t * t;
+        return alpha * t2 * t2 * (2.0 * q + 1.0);
+    } else {
+        if (q < 1.0) return alpha * (1.0 - 1.5 * q * q + 0.75 * q * q * q);
+        double t = 2.0 - q;
+        return alpha * (0.25 * t * t * t);
+    }
+}
+
+template <int KF>
+__device__ __forceinline__ double kernel_dq(double alpha, double q) {
+    if (q >= 2.0) return 0.0;
+    if (KF == NAU_K_WENDLAND) {
+        double t = 1.0 - 0.5 * q;
+        return -5.0 * alpha * q * t * t * t;
+    } else {
+        if (q < 1.0) return alpha * (-3.0 * q + 2.25 * q * q);
+        double t = 2.0 - q;
+        return alpha * (-0.75 * t * t);
+    }
+}
+
+// Kernel::gradient scale (kernel.cpp:62-69): grad = rel * scale; 0 beyond support.
+template <int KF>
+__device__ __forceinline__ double kernel_grad_scale(double alpha, double h, double dist) {
+    double q = dist / h;
+    if (q >= 2.0) return 0.0;
+    return -kernel_dq<KF>(alpha, q) / (h * dist);
+}
+
+template <int DIM>
+__device__ __forceinline__ double norm_rel(const double* r) {
+    double s = r[0] * r[0];
+    if (DIM > 1) s = s + r[1] * r[1];
+    if (DIM > 2) s = s + r[2] * r[2];
+    return sqrt(s);
+}
+
+// ---- neighbour enumeration: include/nauticle/particle_system.hpp:59-138 ----
+// Per axis the options are the surviving direct offsets -1,0,+1 (periodic wrap
+// carries a shift of -/+extent), then mirror-low (cell 0 of a symmetric axis),
+// then mirror-high (cell n-1); axes combine as an odometer, axis 0 fastest.
+struct AxisOpts {
+    int lo_off;  // first direct offset
+    int ndir;    // number of direct options
+    int cnt;     // total options
+};
+
+__device__ __forceinline__ AxisOpts axis_opts(const DomainDev& d, int a, int ci) {
+    AxisOpts o;
+    const int n = d.cells[a];
+    if (d.kind[a] == NAU_PERIODIC) {
+        o.lo_off = -1;
+        o.ndir = 3;
+        o.cnt = 3;
+        return o;
+    }
+    o.lo_off = ci == 0 ? 0 : -1;
+    int hi_off = ci == n - 1 ? 0 : 1;
+    o.ndir = hi_off - o.lo_off + 1;
+    o.cnt = o.ndir;
+    if (d.kind[a] == NAU_SYMMETRIC) {
+        if (ci == 0) o.cnt++;
+        if (ci == n - 1) o.cnt++;
+    }
+    return o;
+}
+
+// Option `o` of axis a: cell, additive shift, reflect (0 direct, -1 low, +1 high).
+__device__ __forceinline__ void axis_opt(const DomainDev& d, int a, int ci, const AxisOpts& ao,
+                                         int o, int& cell, double& shift, int& refl) {
+    const int n = d.cells[a];
+    if (o < ao.ndir) {
+        int c = ci + ao.lo_off + o;
+        shift = 0.0;
+        if (c < 0) {
+            c += n;
+            shift = -d.ext[a];
+        } else if (c >= n) {
+            c -= n;
+            shift = d.ext[a];
+        }
+        cell = c;
+        refl = 0;
+    } else if (o == ao.ndir && ci == 0) {
+        cell = 0;
+        shift = 0.0;
+        refl = -1;
+    } else {
+        cell = n - 1;
+        shift = 0.0;
+        refl = 1;
+    }
+}
+
+__device__ __forceinline__ double image_coord(const DomainDev& d, int a, double xj, double shift,
+                                              int refl) {
+    if (refl == 0) return xj + shift;
+    if (refl < 0) return 2.0 * d.lo[a] - xj;
+    return 2.0 * d.hi[a] - xj;
+}
+
+// Calls fn(j, rel[3], mirror_mask) for every candidate of slot k in reference
+// order; mirror_mask bit a set <=> guide(a) = -1.
+template <int DIM, class Fn>
+__device__ __forceinline__ void for_each_candidate(const Geo& g, int k, const double* xi, Fn&& fn) {
+    const DomainDev& d = g.dom;
+    const int key = g.key[k];
+    int ci[3];
+    ci[0] = key % d.cells[0];
+    ci[1] = DIM > 1 ? (key / d.cells[0]) % d.cells[1] : 0;
+    ci[2] = DIM > 2 ? key / (d.cells[0] * d.cells[1]) : 0;
+    AxisOpts ao[3];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) ao[a] = axis_opts(d, a, ci[a]);
+    const int c2n = DIM > 2 ? ao[2].cnt : 1;
+    const int c1n = DIM > 1 ? ao[1].cnt : 1;
+    for (int o2 = 0; o2 < c2n; ++o2) {
+        int cell2 = 0, refl2 = 0;
+        double sh2 = 0.0;
+        if (DIM > 2) axis_opt(d, 2, ci[2], ao[2], o2, cell2, sh2, refl2);
+        for (int o1 = 0; o1 < c1n; ++o1) {
+            int cell1 = 0, refl1 = 0;
+            double sh1 = 0.0;
+            if (DIM > 1) axis_opt(d, 1, ci[1], ao[1], o1, cell1, sh1, refl1);
+            for (int o0 = 0; o0 < ao[0].cnt; ++o0) {
+                int cell0, refl0;
+                double sh0;
+                axis_opt(d, 0, ci[0], ao[0], o0, cell0, sh0, refl0);
+                int flat = cell0;
+                if (DIM > 1) flat += d.cells[0] * cell1;
+                if (DIM > 2) flat += d.cells[0] * d.cells[1] * cell2;
+                const int mask = (refl0 ? 1 : 0) | (refl1 ? 2 : 0) | (refl2 ? 4 : 0);
+                const int s = g.cell_start[flat];
+                const int e = s + g.cell_count[flat];
+                for (int j = s; j < e; ++j) {
+                    double rel[3] = {0.0, 0.0, 0.0};
+                    rel[0] = image_coord(d, 0, g.x[j], sh0, refl0) - xi[0];
+                    if (fabs(rel[0]) > d.cs[0]) continue;
+                    if (DIM > 1) {
+                        rel[1] = image_coord(d, 1, g.x[g.n + j], sh1, refl1) - xi[1];
+                        if (fabs(rel[1]) > d.cs[1]) continue;
+                    }
+                    if (DIM > 2) {
+                        rel[2] = image_coord(d, 2, g.x[2 * g.n + j], sh2, refl2) - xi[2];
+                        if (fabs(rel[2]) > d.cs[2]) continue;
+                    }
+                    fn(j, rel, mask);
+                }
+            }
+        }
+    }
+}
+
+// mirror() (tensor.cpp:115-126) of component c (column-major, rows x cols).
+__device__ __forceinline__ double mirror_comp(double v, int c, int rows, int cols, int mask,
+                                              int dim) {
+    if (rows == 1 && cols == 1) return v;
+    int r = c % rows, col = c / rows;
+    double srow = (r < dim && ((mask >> r) & 1)) ? -1.0 : 1.0;
+    double scol = (cols == 1 || col >= dim) ? 1.0 : (((mask >> col) & 1) ? -1.0 : 1.0);
+    return v * srow * scol;
+}
+
+}  // namespace nau
+
+// Host-side context (capi.cu owns it; kernels*.cu receive plain arguments).
+struct nau_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool has_domain = false;
+    nau::DomainDev dom{};
+    long n = 0;
+    std::vector<nau::FieldBuf> fields;
+    int* d_orig = nullptr;
+    int* d_orig_s = nullptr;
+    int* d_key = nullptr;
+    int* d_key_s = nullptr;
+    uint8_t* d_active = nullptr;
+    uint8_t* d_active_s = nullptr;
+    int* d_perm = nullptr;
+    int* d_perm_tmp = nullptr;
+    int* d_okey = nullptr;
+    int* d_cell_start = nullptr;  // ncells + 2
+    int* d_cell_count = nullptr;  // ncells + 1
+    int* d_cursor = nullptr;      // ncells + 1
+    int* d_scan_tmp = nullptr;
+    long scan_tmp_len = 0;
+    double* d_red = nullptr;  // reduction scratch
+    nau::DevErr* d_err = nullptr;
+    nau::DevErr* h_err = nullptr;
+    bool dirty = true;
+    bool built_once = false;
+    long rebuild_count = 0;
+    unsigned long long warnings = 0;
+    std::string last_error;
+    long last_bad = -1;
+    long launches = 0;
+    bool profile = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, int>> ev_pairs;  // (class, start event index)
+    int ev_next = 0;
+};
+
+// Launch helpers shared by the .cu files (implemented in capi.cu).
+namespace nau {
+Geo make_geo(nau_ctx* c);
+Opd make_opd(nau_ctx* c, const nau_operand& o);
+void prof_begin(nau_ctx* c, int cls);
+void prof_end(nau_ctx* c, int cls);
+
+// cells.cu
+void launch_boundary_shift(nau_ctx* c);
+void launch_build_cells(nau_ctx* c);
+void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig);
+void launch_unsort(nau_ctx* c, const double* d_src, double* d_dst, int comps);
+void launch_sort_in(nau_ctx* c, const double* d_src_orig, double* d_dst, int comps);
+// interact.cu
+void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int nops,
+                     double* out, int out_rows, int out_cols, int a_rows, int a_cols);
+// integrate.cu
+void launch_euler(nau_ctx* c, const double* x, const double* xdot, double dt, double* out,
+                  int comps);
+void launch_symplectic(nau_ctx* c, double* v, const double* vdot, const double* mask, double dt);
+void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p);
+void launch_reduce(nau_ctx* c, int kind, const double* f, int comps, double* h_out);
+}  // namespace nau

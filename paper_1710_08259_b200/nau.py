@@ -1,0 +1,366 @@
+"""ctypes binding of libnau_b200.so (include/nauticle_gpu.h).
+
+This is the Python face of the C-ABI that tests/, bench.py and smoke() drive.
+It mirrors the reference's host-side vocabulary — Domain, particle fields,
+interaction operators looked up by their SFL names (kOps[],
+/root/reference/proj/src/interactions.cpp:259-269), euler, reductions — and
+raises NauError with the reference's error kinds (include/nauticle/error.hpp).
+
+There is no CPU fallback: importing works anywhere, but creating a Context
+loads the CUDA library and fails loudly if it is missing or no GPU is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnau_b200.so")
+
+PERIODIC, SYMMETRIC, CUTOFF = 0, 1, 2
+OPS = {"sph_S": 0, "sph_D00": 1, "sph_G11": 2, "sph_L0": 3, "sph_A": 4, "dem_l": 5,
+       "dem_boundary_force": 6, "nbody_gravity": 7, "dem_lsd": 8}
+K_WENDLAND, K_CUBIC = 0, 1
+STATUS = {0: "ok", 1: "runtime error", 2: "runtime NaN", 3: "CUDA error", 4: "argument error",
+          5: "communication error"}
+
+# Every symbol include/nauticle_gpu.h declares (checked by tests/test_capi_symbols.py).
+EXPORTS = [
+    "nau_find_interaction", "nau_decode_kernel", "nau_create", "nau_destroy", "nau_set_stream",
+    "nau_get_stream", "nau_set_domain", "nau_set_particles", "nau_particle_count",
+    "nau_active_count", "nau_get_active", "nau_alloc_field", "nau_free_field", "nau_upload",
+    "nau_download", "nau_fill", "nau_copy_field", "nau_field_device_ptr", "nau_boundary_shift",
+    "nau_build_cells", "nau_cells_dirty", "nau_rebuild_count", "nau_warning_count", "nau_ncells",
+    "nau_cell_tables", "nau_neighbor_counts", "nau_interact", "nau_euler", "nau_symplectic_step",
+    "nau_wcsph_step", "nau_reduce", "nau_sync", "nau_last_error", "nau_profile_enable",
+    "nau_profile_ms", "nau_launch_count", "nau_fp64_peak_tflops",
+]
+
+
+class NauError(RuntimeError):
+    def __init__(self, status, message, particle=-1):
+        super().__init__(f"{STATUS.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+        self.particle = particle
+
+
+class OpInfo(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("op", C.c_int), ("arity_min", C.c_int),
+                ("arity_max", C.c_int), ("kernel_slot", C.c_int), ("radius_slot", C.c_int),
+                ("finite_influence", C.c_int)]
+
+
+class Operand(C.Structure):
+    _fields_ = [("field_id", C.c_int), ("rows", C.c_int), ("cols", C.c_int),
+                ("value", C.c_double * 9)]
+
+
+class WcsphParams(C.Structure):
+    _fields_ = [("kernel_family", C.c_int), ("kernel_dim", C.c_int), ("mass", C.c_double),
+                ("radius", C.c_double), ("rho0", C.c_double), ("B", C.c_double),
+                ("gamma", C.c_double), ("visc", C.c_double), ("dt", C.c_double),
+                ("g", C.c_double * 3), ("f_rho", C.c_int), ("f_p", C.c_int), ("f_v", C.c_int),
+                ("f_vdot", C.c_int), ("f_mask", C.c_int)]
+
+
+_lib = None
+
+
+def load():
+    """Load the CUDA library (raises if it was not built: no fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i, d, l = C.c_void_p, C.c_int, C.c_double, C.c_long
+    sig = {
+        "nau_find_interaction": (i, [C.c_char_p, C.POINTER(OpInfo)]),
+        "nau_decode_kernel": (i, [C.c_char_p, C.POINTER(i), C.POINTER(i)]),
+        "nau_create": (i, [i, C.POINTER(vp)]),
+        "nau_destroy": (None, [vp]),
+        "nau_set_stream": (i, [vp, vp]),
+        "nau_get_stream": (vp, [vp]),
+        "nau_set_domain": (i, [vp, i, vp, vp, vp, vp]),
+        "nau_set_particles": (i, [vp, l, vp]),
+        "nau_particle_count": (l, [vp]),
+        "nau_active_count": (l, [vp]),
+        "nau_get_active": (i, [vp, vp]),
+        "nau_alloc_field": (i, [vp, i, i, C.POINTER(i)]),
+        "nau_free_field": (i, [vp, i]),
+        "nau_upload": (i, [vp, i, vp, l]),
+        "nau_download": (i, [vp, i, vp, l]),
+        "nau_fill": (i, [vp, i, vp]),
+        "nau_copy_field": (i, [vp, i, i]),
+        "nau_field_device_ptr": (i, [vp, i, C.POINTER(vp)]),
+        "nau_boundary_shift": (i, [vp]),
+        "nau_build_cells": (i, [vp]),
+        "nau_cells_dirty": (i, [vp]),
+        "nau_rebuild_count": (l, [vp]),
+        "nau_warning_count": (l, [vp]),
+        "nau_ncells": (l, [vp]),
+        "nau_cell_tables": (i, [vp, vp, vp, vp, vp]),
+        "nau_neighbor_counts": (i, [vp, d, vp]),
+        "nau_interact": (i, [vp, i, i, i, C.POINTER(Operand), i, i]),
+        "nau_euler": (i, [vp, i, i, d, i]),
+        "nau_symplectic_step": (i, [vp, i, i, i, d]),
+        "nau_wcsph_step": (i, [vp, C.POINTER(WcsphParams)]),
+        "nau_reduce": (i, [vp, i, i, vp]),
+        "nau_sync": (i, [vp]),
+        "nau_last_error": (C.c_char_p, [vp, C.POINTER(l)]),
+        "nau_profile_enable": (i, [vp, i]),
+        "nau_profile_ms": (d, [vp, i, C.POINTER(l)]),
+        "nau_launch_count": (l, [vp]),
+        "nau_fp64_peak_tflops": (d, [i]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def find_interaction(name):
+    """≙ find_interaction (interactions.cpp:273-277); returns the kOps[] row as a dict."""
+    L = load()
+    info = OpInfo()
+    if L.nau_find_interaction(name.encode(), C.byref(info)) != 0:
+        raise NauError(4, L.nau_last_error(None, None).decode())
+    return {"name": info.name.decode(), "op": info.op, "arity_min": info.arity_min,
+            "arity_max": info.arity_max, "kernel_slot": info.kernel_slot,
+            "radius_slot": info.radius_slot, "finite_influence": bool(info.finite_influence)}
+
+
+def decode_kernel(keyword):
+    """≙ decode_kernel_keyword (kernel.cpp:20-35), plus the cubic-spline family Wc3D220."""
+    L = load()
+    fam, dim = C.c_int(0), C.c_int(0)
+    if L.nau_decode_kernel(keyword.encode(), C.byref(fam), C.byref(dim)) != 0:
+        raise NauError(4, L.nau_last_error(None, None).decode())
+    return fam.value, dim.value
+
+
+def fp64_peak_tflops(device=0):
+    return load().nau_fp64_peak_tflops(device)
+
+
+class Field:
+    def __init__(self, ctx, fid, rows, cols):
+        self.ctx, self.id, self.rows, self.cols = ctx, fid, rows, cols
+
+    @property
+    def comps(self):
+        return self.rows * self.cols
+
+
+class Context:
+    """One GPU context: domain, particles (field 0 = r) and SoA fields on the device."""
+
+    def __init__(self, device=0):
+        self.L = load()
+        h = C.c_void_p()
+        st = self.L.nau_create(device, C.byref(h))
+        if st != 0:
+            raise NauError(st, self.L.nau_last_error(None, None).decode())
+        self.h = h
+        self.n = 0
+        self.dim = 0
+        self.fields = {}
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.nau_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != 0:
+            bad = C.c_long(-1)
+            msg = self.L.nau_last_error(self.h, C.byref(bad)).decode()
+            raise NauError(st, msg, bad.value)
+
+    # ---- setup ----
+    def set_stream(self, stream_ptr):
+        self._check(self.L.nau_set_stream(self.h, C.c_void_p(stream_ptr)))
+
+    def set_domain(self, dim, min_cells, max_cells, cell_size, kinds):
+        pad = lambda v, f, t: np.array(list(v) + [f] * (3 - len(v)), t)
+        self._dom = (pad(min_cells, 0, np.int32), pad(max_cells, 1, np.int32),
+                     pad(cell_size, 1.0, np.float64), pad(kinds, CUTOFF, np.int32))
+        self._check(self.L.nau_set_domain(self.h, dim, *[_p(a) for a in self._dom]))
+        self.dim = dim
+
+    def set_particles(self, pos):
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        assert pos.shape[0] == self.dim
+        self.n = pos.shape[1]
+        self._check(self.L.nau_set_particles(self.h, self.n, _p(pos)))
+        self.fields = {"r": Field(self, 0, self.dim, 1)}
+        return self.fields["r"]
+
+    def add_field(self, name, rows=1, cols=1, values=None):
+        fid = C.c_int(-1)
+        self._check(self.L.nau_alloc_field(self.h, rows, cols, C.byref(fid)))
+        f = Field(self, fid.value, rows, cols)
+        self.fields[name] = f
+        if values is not None:
+            a = np.asarray(values, dtype=np.float64)
+            if a.ndim >= 1 and a.shape[-1] == self.n and a.size == rows * cols * self.n:
+                self.upload(f, a)
+            else:
+                self.fill(f, a)
+        return f
+
+    def field(self, name):
+        return self.fields[name]
+
+    def _fid(self, f):
+        if isinstance(f, Field):
+            return f.id
+        if isinstance(f, str):
+            return self.fields[f].id
+        return int(f)
+
+    def _comps(self, f):
+        f = self.fields[f] if isinstance(f, str) else f
+        return f.comps
+
+    def upload(self, f, values):
+        a = np.ascontiguousarray(np.asarray(values, dtype=np.float64).reshape(-1, self.n))
+        self._check(self.L.nau_upload(self.h, self._fid(f), _p(a), self.n))
+
+    def upload_ptr(self, f, host_ptr):
+        """Upload from a raw host pointer (e.g. a pinned torch tensor's data_ptr())."""
+        self._check(self.L.nau_upload(self.h, self._fid(f), C.c_void_p(host_ptr), self.n))
+
+    def download(self, f):
+        out = np.empty((self._comps(f), self.n), np.float64)
+        self._check(self.L.nau_download(self.h, self._fid(f), _p(out), self.n))
+        return out
+
+    def download_ptr(self, f, host_ptr):
+        self._check(self.L.nau_download(self.h, self._fid(f), C.c_void_p(host_ptr), self.n))
+
+    def fill(self, f, value):
+        v = np.zeros(9)
+        vv = np.atleast_1d(np.asarray(value, dtype=np.float64)).ravel()
+        v[: vv.size] = vv
+        self._check(self.L.nau_fill(self.h, self._fid(f), _p(v)))
+
+    def device_ptr(self, f):
+        p = C.c_void_p()
+        self._check(self.L.nau_field_device_ptr(self.h, self._fid(f), C.byref(p)))
+        return p.value
+
+    # ---- ParticleSystem ----
+    def boundary_shift(self):
+        self._check(self.L.nau_boundary_shift(self.h))
+
+    def build_cells(self):
+        self._check(self.L.nau_build_cells(self.h))
+
+    @property
+    def ncells(self):
+        return self.L.nau_ncells(self.h)
+
+    @property
+    def rebuild_count(self):
+        return self.L.nau_rebuild_count(self.h)
+
+    @property
+    def warning_count(self):
+        return self.L.nau_warning_count(self.h)
+
+    def active(self):
+        out = np.empty(self.n, np.uint8)
+        self._check(self.L.nau_get_active(self.h, _p(out)))
+        return out
+
+    def active_count(self):
+        return self.L.nau_active_count(self.h)
+
+    def cell_tables(self):
+        nc = self.ncells
+        cell_of = np.empty(self.n, np.int32)
+        start = np.empty(nc, np.int32)
+        count = np.empty(nc, np.int32)
+        srt = np.empty(max(1, self.n), np.int32)
+        self._check(self.L.nau_cell_tables(self.h, _p(cell_of), _p(start), _p(count), _p(srt)))
+        return cell_of, start, count, srt[: int(count.sum())].copy()
+
+    def neighbor_counts(self, radius):
+        out = np.empty(self.n, np.int32)
+        self._check(self.L.nau_neighbor_counts(self.h, float(radius), _p(out)))
+        return out
+
+    # ---- operators ----
+    def _operand(self, o):
+        x = Operand()
+        if isinstance(o, (Field, str)):
+            f = self.fields[o] if isinstance(o, str) else o
+            x.field_id, x.rows, x.cols = f.id, f.rows, f.cols
+        else:
+            v = np.atleast_1d(np.asarray(o, dtype=np.float64)).ravel()
+            x.field_id, x.rows, x.cols = -1, v.size, 1
+            for k, val in enumerate(v):
+                x.value[k] = val
+        return x
+
+    def interact(self, name, operands, out, kernel=None):
+        """Evaluate SFL operator `name` for all particles into field `out`.
+
+        operands: the kOps[] operand list WITHOUT the kernel keyword (fields by
+        name/Field, uniforms as numbers or tuples); kernel: keyword such as
+        "Wp53220" or "Wc33220" for SPH operators.
+        """
+        op = OPS[name]
+        kf, kd = (K_WENDLAND, self.dim) if kernel is None else decode_kernel(kernel)
+        arr = (Operand * len(operands))(*[self._operand(o) for o in operands])
+        self._check(self.L.nau_interact(self.h, op, kf, kd, arr, len(operands), self._fid(out)))
+
+    def euler(self, x, xdot, dt, out):
+        self._check(self.L.nau_euler(self.h, self._fid(x), self._fid(xdot), float(dt),
+                                     self._fid(out)))
+
+    def symplectic_step(self, v, vdot, mask, dt):
+        self._check(self.L.nau_symplectic_step(self.h, self._fid(v), self._fid(vdot),
+                                               -1 if mask is None else self._fid(mask), float(dt)))
+
+    def wcsph_step(self, p: WcsphParams):
+        self._check(self.L.nau_wcsph_step(self.h, C.byref(p)))
+
+    def reduce(self, kind, f):
+        kinds = {"fmax": 0, "fmin": 1, "fsum": 2, "fmean": 3}
+        out = np.zeros(9)
+        self._check(self.L.nau_reduce(self.h, kinds[kind], self._fid(f), _p(out)))
+        return out[: (self._comps(f) if kinds[kind] >= 2 else 1)]
+
+    def sync(self):
+        self._check(self.L.nau_sync(self.h))
+
+    # ---- instrumentation ----
+    def profile(self, on=True):
+        self._check(self.L.nau_profile_enable(self.h, 1 if on else 0))
+
+    def profile_ms(self, cls=1):
+        cnt = C.c_long(0)
+        ms = self.L.nau_profile_ms(self.h, cls, C.byref(cnt))
+        return ms, cnt.value
+
+    @property
+    def launches(self):
+        return self.L.nau_launch_count(self.h)

@@ -1,0 +1,155 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations.
+
+No dataset is involved: every input is generated here. Random draws use the
+reference's counter RNG (RandomState, /root/reference/proj/include/nauticle/
+sfl/random_state.hpp:22-41), restated vectorised so that draw k of particle i
+equals the reference's k-th ``rand`` call at particle i (pinned in
+tests/test_oracle.py against oracle/_ref).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _mix(x):
+    x = x + np.uint64(0x9E3779B97F4A7C15)
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def uniform_draws(seed: int, n: int, ndraws: int, a=0.0, b=1.0) -> np.ndarray:
+    """out[k, i] = RandomState(seed).uniform(i, a, b) at its k-th call for particle i."""
+    with np.errstate(over="ignore"):
+        s = _mix(np.uint64(seed) ^ np.uint64(0x6E61757469636C65))
+        pi = _mix(np.arange(n, dtype=np.uint64) + np.uint64(0x9E3779B9))
+        out = np.empty((ndraws, n), np.float64)
+        for k in range(ndraws):
+            x = _mix(s ^ pi ^ np.uint64(k))
+            u = (x >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+            out[k] = a + u * (b - a)
+    return out
+
+
+@dataclass
+class Scene:
+    name: str
+    dim: int
+    min_cells: list
+    max_cells: list
+    cell_size: list
+    kinds: list
+    pos: np.ndarray                      # (dim, n)
+    fields: dict = field(default_factory=dict)   # name -> (comps, n) or (n,)
+    params: dict = field(default_factory=dict)
+
+    @property
+    def n(self):
+        return self.pos.shape[1]
+
+
+# ---------------------------------------------------------------- cfg1 ----
+def sph_microbench(n=1_048_576, seed=1, neighbours=50.0, rho0=1000.0) -> Scene:
+    """BASELINE cfg1: N uniform-random particles in the periodic unit cube.
+
+    2h is chosen so the expected neighbour count within 2h is `neighbours`
+    (excluding self): (4/3) pi (2h)^3 N = neighbours. The domain needs an
+    integer number of cells (domain.hpp:26-30): floor(1/2h) cells of 1/that.
+    Draws 0,1,2 of particle i are x,y,z; draw 3 is the scalar field A.
+    """
+    two_h = (3.0 * neighbours / (4.0 * math.pi * n)) ** (1.0 / 3.0)
+    cells = int(math.floor(1.0 / two_h))
+    cs = 1.0 / cells
+    d = uniform_draws(seed, n, 4)
+    # draws are in [0,1); the computed domain is [0, cells*cs) (== 1.0 for 44 cells)
+    hi = cells * cs
+    pos = np.ascontiguousarray(d[:3] * hi if hi != 1.0 else d[:3])
+    return Scene("sph_microbench", 3, [0, 0, 0], [cells] * 3, [cs] * 3, [0, 0, 0], pos,
+                 fields={"A": d[3].copy()},
+                 params={"radius": two_h, "h": 0.5 * two_h, "mass": rho0 / n, "rho0": rho0})
+
+
+# ------------------------------------------------------------ cfg0 / cfg2 ----
+def _lattice(box_lo, box_hi, dx):
+    """Cell-centred lattice points ((i+1/2) dx per axis) of an index box [lo, hi)."""
+    axes = [(np.arange(l, h, dtype=np.float64) + 0.5) * dx for l, h in zip(box_lo, box_hi)]
+    if any(len(a) == 0 for a in axes):
+        return np.zeros((len(axes), 0))
+    mesh = np.meshgrid(*axes, indexing="ij")
+    # axis 0 fastest in the flattened order
+    return np.stack([m.transpose(tuple(range(len(axes)))[::-1]).ravel() for m in mesh])
+
+
+def dam_break(dim=2, dx=0.01, fluid=None, tank=None, layers=3, rho0=1000.0, gravity=9.81,
+              alpha=0.02, cfl=0.2, gamma=7.0, kernel_family=0) -> Scene:
+    """BASELINE cfg0 (2D, defaults) / cfg2 (dim=3, dx=0.005): WCSPH dam break.
+
+    Fluid block at ((i+1/2)dx, ...) from the origin; `layers` of fixed wall
+    particles on the floor and the side walls of the tank (open top). Wendland
+    C2 with h = 2 dx, cell size 2h, Tait EOS with c0 = 10 sqrt(2 g H), gamma = 7,
+    artificial viscosity alpha, dt = cfl h / c0. Walls carry mask 0.
+    """
+    if fluid is None:
+        fluid = (1.0, 2.0) if dim == 2 else (1.0, 0.5, 1.0)
+    if tank is None:
+        tank = (4.0, 3.0) if dim == 2 else (3.2, 1.0, 1.5)
+    nf = [int(round(f / dx)) for f in fluid]
+    nt = [int(round(t / dx)) for t in tank]
+    fpos = _lattice([0] * dim, nf, dx)
+    L = layers
+    boxes = []
+    if dim == 2:
+        boxes.append(([-L, -L], [nt[0] + L, 0]))          # floor incl. corners
+        boxes.append(([-L, 0], [0, nt[1]]))               # left wall
+        boxes.append(([nt[0], 0], [nt[0] + L, nt[1]]))    # right wall
+    else:
+        boxes.append(([-L, -L, -L], [nt[0] + L, nt[1] + L, 0]))
+        boxes.append(([-L, -L, 0], [0, nt[1] + L, nt[2]]))
+        boxes.append(([nt[0], -L, 0], [nt[0] + L, nt[1] + L, nt[2]]))
+        boxes.append(([0, -L, 0], [nt[0], 0, nt[2]]))
+        boxes.append(([0, nt[1], 0], [nt[0], nt[1] + L, nt[2]]))
+    wpos = np.concatenate([_lattice(lo, hi, dx) for lo, hi in boxes], axis=1)
+    pos = np.ascontiguousarray(np.concatenate([fpos, wpos], axis=1))
+    n_f, n = fpos.shape[1], pos.shape[1]
+    h = 2.0 * dx
+    radius = 2.0 * h
+    cell = radius
+    H = fluid[-1]
+    c0 = 10.0 * math.sqrt(2.0 * gravity * H)
+    B = c0 * c0 * rho0 / gamma
+    mass = rho0 * dx ** dim
+    dt = cfl * h / c0
+    g = [0.0] * dim
+    g[-1] = -gravity
+    max_cells = [int(math.ceil(t / cell - 1e-9)) + 1 for t in tank]
+    min_cells = [-1] * dim
+    mask = np.zeros(n)
+    mask[:n_f] = 1.0
+    # initial hydrostatic density via the inverse Tait EOS (walls at rho0)
+    rho = np.full(n, rho0)
+    depth = H - fpos[-1]
+    rho[:n_f] = rho0 * (1.0 + rho0 * gravity * depth / B) ** (1.0 / gamma)
+    return Scene(
+        f"dam_break_{dim}d", dim, min_cells, max_cells, [cell] * dim, [2] * dim, pos,
+        fields={"rho": rho, "p": np.zeros(n), "v": np.zeros((dim, n)), "vdot": np.zeros((dim, n)),
+                "mask": mask},
+        params={"dx": dx, "h": h, "radius": radius, "mass": mass, "rho0": rho0, "c0": c0, "B": B,
+                "gamma": gamma, "alpha": alpha, "visc": alpha * c0 * h, "dt": dt, "g": g,
+                "n_fluid": n_f, "kernel_family": kernel_family})
+
+
+def wcsph_equations(scene: Scene, kernel_keyword=None):
+    """The dam-break deck as SFL equation text (for the reference oracle)."""
+    kw = kernel_keyword or f"Wp5{scene.dim}220"
+    return [
+        ("density", f"rho=sph_S(one,mass,one,{kw},R)"),
+        ("eos", "p=B*((rho/rho0)^gam-1)"),
+        ("momentum", f"vdot=-1/rho*sph_G11(p,mass,rho,{kw},R)+visc*sph_A(v,mass,rho,{kw},R)+g"),
+        ("velocity", "v=euler(v,vdot*mask,dt)"),
+        ("position", "r=euler(r,v,dt)"),
+    ]

@@ -1,0 +1,277 @@
+"""GPU parity tests: the CUDA path through the C-ABI vs the oracle.
+
+Integer data (cell ids, cell tables, sorted order, neighbour counts) must be
+bit-exact. The SPH operators and the linear spring-dashpot law are compiled
+without FMA contraction and sum in the reference's candidate order, so they
+are checked bitwise too. Paths through a libm transcendental (Hertz pow,
+gravity's r^1.5, the Tait EOS pow) use BASELINE's fp64 tolerance: 1e-10
+relative for one step, 1e-6 relative after 10 steps (north_star).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import cases
+import deck_oracle
+from oracle import port
+from paper_1710_08259_b200 import nau, scenes
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL_STEP = 1e-10
+TOL_10 = 1e-6
+TRANSCENDENTAL = {"dem_l", "dem_boundary_force", "nbody_gravity"}
+
+
+def rel_err(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    scale = max(np.abs(b).max(initial=0.0), 1e-300)
+    return float(np.abs(a - b).max(initial=0.0) / scale)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = nau.Context(0)
+    yield c
+    c.close()
+
+
+def unpack_spec(z, p):
+    meta = json.loads(str(z[p + "meta"]))
+    spec = {k: meta[k] for k in ("dim", "min_cells", "max_cells", "cell_size", "kinds")}
+    spec["consts"] = meta["consts"]
+    spec["pos"] = z[p + "pos"]
+    spec["fields"] = {k: z[p + "f_" + k] for k in meta["fields"]}
+    return spec
+
+
+def check_against(spec, ctx, expect_tables, expect_counts, expect_ops):
+    cases.gpu_context(spec, ctx)
+    tables = ctx.cell_tables()
+    for got, exp, name in zip(tables, expect_tables, ("cell_of", "start", "count", "sorted")):
+        np.testing.assert_array_equal(got, exp, err_msg=name)
+    np.testing.assert_array_equal(ctx.neighbor_counts(spec["consts"]["R"]), expect_counts)
+    for entry, exp in zip(cases.op_list(spec["dim"]), expect_ops):
+        if exp is None:
+            continue
+        got = cases.gpu_eval(spec, ctx, entry)
+        if entry[0] in TRANSCENDENTAL:
+            assert rel_err(got, exp) <= TOL_STEP, entry[0]
+        else:
+            np.testing.assert_array_equal(got, exp, err_msg=f"{entry[0]} {entry[2]}")
+
+
+@pytest.mark.parametrize("idx", range(16))
+def test_golden_random_cases(ctx, idx):
+    z = np.load(os.path.join(GOLD, "random_cases.npz"))
+    if idx >= int(z["n_random_cases"]):
+        pytest.skip()
+    p = f"c{idx}_"
+    spec = unpack_spec(z, p)
+    ops = [None if p + f"op{k}_error" in z else z[p + f"op{k}"]
+           for k in range(len(cases.op_list(spec["dim"])))]
+    check_against(spec, ctx, [z[p + s] for s in ("cell_of", "cell_start", "cell_count", "sorted")],
+                  z[p + "counts"], ops)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_live_random_cases_vs_port(ctx, seed):
+    rng = np.random.default_rng(77 + seed)
+    spec = cases.random_spec(rng, n=int(rng.integers(500, 3000)), cells=None)
+    ps = cases.port_system(spec)
+    ops = [cases.port_eval(spec, ps, e) for e in cases.op_list(spec["dim"])]
+    check_against(spec, ctx, ps.tables, ps.neighbor_counts(spec["consts"]["R"]), ops)
+
+
+def test_edge_layouts(ctx):
+    rng = np.random.default_rng(5)
+    # everything in one cell (large ppc), periodic 1-cell axes visited three times
+    spec = cases.random_spec(rng, dim=3, n=1500, kinds=[0, 0, 0], cells=[1, 1, 1])
+    ps = cases.port_system(spec)
+    ops = [cases.port_eval(spec, ps, e) for e in cases.op_list(3)]
+    check_against(spec, ctx, ps.tables, ps.neighbor_counts(spec["consts"]["R"]), ops)
+    # particles exactly on cell faces and on the periodic seam
+    spec = cases.random_spec(rng, dim=2, n=400, kinds=[0, 1], cells=[4, 3])
+    pos = spec["pos"]
+    pos[0, :100] = np.round(pos[0, :100] / 0.3) * 0.3
+    pos[0, 100:110] = np.nextafter(1.2, 0.0)
+    pos[1, 110:130] = 0.0
+    ps = cases.port_system(spec)
+    ops = [cases.port_eval(spec, ps, e) for e in cases.op_list(2)]
+    check_against(spec, ctx, ps.tables, ps.neighbor_counts(spec["consts"]["R"]), ops)
+
+
+def test_empty_and_single(ctx):
+    rng = np.random.default_rng(6)
+    spec = cases.random_spec(rng, dim=2, n=0, kinds=[0, 2], cells=[3, 2])
+    cases.gpu_context(spec, ctx)
+    cell_of, start, count, srt = ctx.cell_tables()
+    assert count.sum() == 0 and len(srt) == 0 and (start == 0).all()
+    spec = cases.random_spec(rng, dim=3, n=1, kinds=[1, 1, 1], cells=[1, 1, 1])
+    ps = cases.port_system(spec)
+    ops = [cases.port_eval(spec, ps, e) for e in cases.op_list(3)]
+    check_against(spec, ctx, ps.tables, ps.neighbor_counts(spec["consts"]["R"]), ops)
+
+
+def test_cutoff_leavers_are_deactivated_and_frozen(ctx):
+    rng = np.random.default_rng(8)
+    spec = cases.random_spec(rng, dim=2, n=600, kinds=[2, 0], cells=[5, 4])
+    spec["pos"][0, :37] = -0.05   # outside the cut-off face: deactivated by the shift
+    spec["pos"][0, 37:50] = 1.52  # beyond hi = 1.5
+    ps = cases.port_system(spec)
+    assert ps.active.sum() == 550
+    cases.gpu_context(spec, ctx)
+    np.testing.assert_array_equal(ctx.active(), ps.active)
+    ops = [cases.port_eval(spec, ps, e) for e in cases.op_list(2)]
+    check_against(spec, ctx, ps.tables, ps.neighbor_counts(spec["consts"]["R"]), ops)
+
+
+def test_errors_surface_like_the_reference(ctx):
+    rng = np.random.default_rng(9)
+    spec = cases.random_spec(rng, dim=2, n=300, kinds=[0, 0], cells=[4, 4])
+    spec["fields"]["rho"][0, 17] = 0.0
+    cases.gpu_context(spec, ctx)
+    ctx.add_field("o", 2, 1, 0.0)
+    ctx.interact("sph_G11", ["A", 0.5, "rho", 0.3], "o", kernel="Wp52220")
+    with pytest.raises(nau.NauError) as e:  # interactions.cpp:92-94 zero density
+        ctx.sync()
+    assert e.value.status == 1 and "zero density" in e.value.message
+    ctx.interact("sph_S", ["A", 0.5, "rho", -1.0], "o1" if "o1" in ctx.fields else
+                 ctx.add_field("o1", 1, 1, 0.0), kernel="Wp52220")
+    with pytest.raises(nau.NauError) as e:  # sph_context radius check
+        ctx.sync()
+    assert "radius" in e.value.message
+    with pytest.raises(nau.NauError):  # D00 needs a vector operand
+        ctx.interact("sph_D00", ["A", 0.5, "rho", 0.3], "o1", kernel="Wp52220")
+    nan = spec["fields"]["A"].copy()
+    nan[0, 5] = np.nan
+    ctx.add_field("An", 1, 1, nan)
+    ctx.interact("sph_L0", ["An", 0.5, 1000.0, 0.3], "o1", kernel="Wp52220")
+    with pytest.raises(nau.NauError) as e:  # case.cpp:46-53 NaN audit
+        ctx.sync()
+    assert e.value.status == 2
+    ctx.sync()  # error word cleared
+
+
+def test_microbench_golden(ctx):
+    z = np.load(os.path.join(GOLD, "microbench_small.npz"))
+    sc = scenes.sph_microbench(n=int(z["mb_n"]))
+    prm = sc.params
+    ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+    ctx.set_particles(sc.pos)
+    ctx.add_field("A", 1, 1, sc.fields["A"])
+    ctx.add_field("rho", 1, 1, 0.0)
+    ctx.add_field("G", 3, 1, 0.0)
+    ctx.add_field("L", 1, 1, 0.0)
+    ctx.boundary_shift()
+    _, start, _, srt = ctx.cell_tables()
+    np.testing.assert_array_equal(start, z["mb_cell_start"])
+    np.testing.assert_array_equal(srt, z["mb_sorted"])
+    np.testing.assert_array_equal(ctx.neighbor_counts(prm["radius"]), z["mb_counts"])
+    ctx.add_field("rho_w", 1, 1, z["mb_rho_w"])
+    for kw, sfx in (("Wp53220", "w"), ("Wc33220", "c")):
+        ctx.interact("sph_S", [1.0, prm["mass"], 1.0, prm["radius"]], "rho", kernel=kw)
+        ctx.interact("sph_G11", ["A", prm["mass"], "rho_w", prm["radius"]], "G", kernel=kw)
+        ctx.interact("sph_L0", ["A", prm["mass"], "rho_w", prm["radius"]], "L", kernel=kw)
+        np.testing.assert_array_equal(ctx.download("rho"), z["mb_rho_" + sfx])
+        np.testing.assert_array_equal(ctx.download("G"), z["mb_G_" + sfx])
+        np.testing.assert_array_equal(ctx.download("L"), z["mb_L_" + sfx])
+
+
+def test_microbench_full_size(ctx):
+    """BASELINE cfg1 at its full N = 1,048,576: bit-exact tables and counts, bitwise density."""
+    sc = scenes.sph_microbench()
+    prm = sc.params
+    ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+    ctx.set_particles(sc.pos)
+    ctx.add_field("rho", 1, 1, 0.0)
+    ctx.boundary_shift()
+    dom = port.Domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+    ps = port.ParticleSystem(dom, sc.pos)
+    ps.boundary_shift()
+    ps.build_cells()
+    for got, exp in zip(ctx.cell_tables(), ps.tables):
+        np.testing.assert_array_equal(got, exp)
+    counts = ctx.neighbor_counts(prm["radius"])
+    np.testing.assert_array_equal(counts, ps.neighbor_counts(prm["radius"]))
+    assert abs(counts.mean() - 51.0) < 0.5  # 50 expected neighbours + self
+    ctx.interact("sph_S", [1.0, prm["mass"], 1.0, prm["radius"]], "rho", kernel="Wc33220")
+    rho = ctx.download("rho")
+    np.testing.assert_array_equal(
+        rho, ps.interact(port.SPH_S, [1.0, prm["mass"], 1.0, prm["radius"]], (1, 1),
+                         kfamily=port.K_CUBIC))
+
+
+def _gpu_dam(ctx, sc):
+    prm = sc.params
+    ctx.set_domain(sc.dim, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+    ctx.set_particles(sc.pos)
+    for k in ("rho", "p", "v", "vdot", "mask"):
+        v = np.asarray(sc.fields[k]).reshape(-1, sc.n)
+        ctx.add_field(k, v.shape[0], 1, v)
+    ctx.boundary_shift()
+    p = nau.WcsphParams()
+    p.kernel_family, p.kernel_dim = nau.K_WENDLAND, sc.dim
+    p.mass, p.radius, p.rho0, p.B = prm["mass"], prm["radius"], prm["rho0"], prm["B"]
+    p.gamma, p.visc, p.dt = prm["gamma"], prm["visc"], prm["dt"]
+    for a in range(sc.dim):
+        p.g[a] = prm["g"][a]
+    f = ctx.fields
+    p.f_rho, p.f_p, p.f_v, p.f_vdot, p.f_mask = (f["rho"].id, f["p"].id, f["v"].id,
+                                                 f["vdot"].id, f["mask"].id)
+    return p
+
+
+def test_dam_break_small_vs_reference_golden(ctx):
+    z = np.load(os.path.join(GOLD, "dam_break_2d_small.npz"))
+    meta = json.loads(str(z["dam_meta"]))
+    sc = scenes.dam_break(2, dx=meta["dx"], fluid=tuple(meta["fluid"]), tank=tuple(meta["tank"]))
+    p = _gpu_dam(ctx, sc)
+    for s in range(1, meta["steps"] + 1):
+        ctx.wcsph_step(p)
+        if s in (1, meta["steps"]):
+            tol = TOL_STEP if s == 1 else TOL_10
+            assert rel_err(ctx.download("r"), z[f"dam_s{s}_r"]) <= tol
+            for k in ("rho", "p", "v", "vdot"):
+                assert rel_err(ctx.download(k), z[f"dam_s{s}_{k}"]) <= tol, (s, k)
+            np.testing.assert_array_equal(ctx.active(), z[f"dam_s{s}_active"])
+
+
+def test_dam_break_cfg0_full_vs_port_10_steps(ctx):
+    """BASELINE cfg0 (23,018 particles): 1 step within 1e-10, 10 steps within 1e-6,
+    mass exactly conserved (no particle lost), momentum consistent."""
+    sc = scenes.dam_break(2)
+    prm = sc.params
+    p = _gpu_dam(ctx, sc)
+    ps, st = deck_oracle.make_system(sc)
+    for s in range(1, 11):
+        ctx.wcsph_step(p)
+        deck_oracle.step(ps, st, prm)
+        if s in (1, 10):
+            tol = TOL_STEP if s == 1 else TOL_10
+            assert rel_err(ctx.download("r"), ps.pos) <= tol
+            for k in ("rho", "p", "v"):
+                assert rel_err(ctx.download(k), st[k]) <= tol, (s, k)
+    act = ctx.active()
+    np.testing.assert_array_equal(act, ps.active)
+    assert act.sum() * prm["mass"] == sc.n * prm["mass"]  # mass conserved exactly
+    mom_g = (ctx.download("v") * prm["mass"]).sum(axis=1)
+    mom_o = (st["v"] * prm["mass"]).sum(axis=1)
+    assert np.abs(mom_g - mom_o).max() <= 1e-8 * max(np.abs(mom_o).max(), 1e-30)
+
+
+def test_euler_and_reduce(ctx):
+    rng = np.random.default_rng(12)
+    spec = cases.random_spec(rng, dim=3, n=2000, kinds=[0, 1, 2], cells=[3, 3, 3])
+    cases.gpu_context(spec, ctx)
+    ctx.add_field("V2", 3, 1, 0.0)
+    ctx.euler("V", "V", 0.25, "V2")
+    V = spec["fields"]["V"]
+    np.testing.assert_array_equal(ctx.download("V2"), V + 0.25 * V)
+    s = ctx.reduce("fsum", "A")
+    assert abs(s[0] - spec["fields"]["A"].sum()) <= 1e-12 * spec["fields"]["A"].sum()
+    assert ctx.reduce("fmax", "A")[0] == spec["fields"]["A"].max()
+    nrm = np.sqrt((V * V).sum(axis=0))
+    assert ctx.reduce("fmin", "V")[0] == pytest.approx(nrm.min(), rel=1e-15)
