@@ -392,6 +392,8 @@ def run_ours(args, dist):
     torch.cuda.synchronize()
     dist.barrier()
     prof = {cls: ctx.profile_ms(cls) for cls in wl.kernels}
+    if not any(c for _, c in prof.values()):
+        print("profile empty:", prof, ctx.L.nau_last_error(ctx.h, None), file=sys.stderr)
     ctx.profile(False)
     ms_max = dist.max(ms)
     n_total = dist.sum(float(wl.n_active))

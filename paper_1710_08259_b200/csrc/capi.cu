@@ -680,9 +680,12 @@ double nau_profile_ms(nau_ctx* c, int cls, long* launches) {
     for (auto& pr : c->ev_pairs) {
         if (pr.first != cls) continue;
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, c->ev_pool[pr.second], c->ev_pool[pr.second + 1]) == cudaSuccess) {
+        cudaError_t e = cudaEventElapsedTime(&ms, c->ev_pool[pr.second], c->ev_pool[pr.second + 1]);
+        if (e == cudaSuccess) {
             total += ms;
             ++cnt;
+        } else {
+            c->last_error = std::string("profile: ") + cudaGetErrorString(e);
         }
     }
     if (launches) *launches = cnt;

@@ -46,7 +46,9 @@ __global__ void __launch_bounds__(kThreads) k_sph(const __grid_constant__ SphArg
     }
     const double h = 0.5 * radius;
     const double alpha = kernel_alpha<KF>(a.kdim, h);
-    const int ac = AC == 1 ? 1 : a.arows * a.acols;
+    // components of A held per particle: S any shape, D00/A a d-vector, G11/L0 scalar
+    const int ac = OP == NAU_OP_SPH_S ? (AC == 1 ? 1 : a.arows * a.acols)
+                                      : ((OP == NAU_OP_SPH_D00 || OP == NAU_OP_SPH_A) ? DIM : 1);
     double a_i[9];
 #pragma unroll
     for (int c = 0; c < 9; ++c) a_i[c] = (c < ac) ? a.A.at(c, k, n) : 0.0;

@@ -113,7 +113,7 @@ def gpu_context(spec, ctx=None):
                    spec["kinds"])
     ctx.set_particles(spec["pos"])
     for k, v in spec["fields"].items():
-        v = np.asarray(v).reshape(-1, spec["pos"].shape[1])
+        v = np.atleast_2d(np.asarray(v))
         ctx.add_field(k, v.shape[0], 1, v)
     ctx.boundary_shift()
     ctx.build_cells()
