@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the bounded reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="fast", choices=["fast", "exact"],
+                    help="fast: warp-per-particle sums (1e-10 tolerance); exact: reference order, bitwise")
     return ap.parse_args()
 
 
@@ -374,6 +376,7 @@ def run_ours(args, dist):
 
     wl = make_workload(args.config)
     ctx = nau.Context(dist.local)
+    ctx.set_mode(args.mode == "fast")
     wl.setup(ctx)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=f"cuda:{dist.local}")
     for _ in range(args.warmup):
@@ -439,7 +442,8 @@ def run_ours(args, dist):
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(wl.config(), parallelism="replicas" if dist.world > 1 else "single GPU",
+        "config": dict(wl.config(), mode=args.mode,
+                       parallelism="replicas" if dist.world > 1 else "single GPU",
                        l2="flushed between timed steps (256 MiB memset, untimed)"),
         "e2e": {"value": round(e2e, 1), "unit": "particle-updates/s",
                 "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h),

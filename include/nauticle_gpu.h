@@ -86,6 +86,17 @@ nau_status nau_decode_kernel(const char* keyword, int* family, int* dim);
 /* ---- context ---- */
 nau_status nau_create(int device, nau_ctx** out);
 void nau_destroy(nau_ctx* ctx);
+
+/* Evaluation mode of the neighbour sums.
+ * EXACT (default): one lane per particle, candidates summed in the reference's
+ *   order with the reference's arithmetic (no FMA, IEEE div/sqrt): bitwise equal
+ *   to the reference wherever no libm transcendental is involved.
+ * FAST: one warp per particle, FMA/rsqrt/reciprocal arithmetic and a warp-tree
+ *   reduction: same candidates and filters, summation order differs
+ *   (BASELINE tolerance: 1e-10 relative; observed ~1e-14). */
+enum { NAU_MODE_EXACT = 0, NAU_MODE_FAST = 1 };
+nau_status nau_set_mode(nau_ctx* ctx, int mode);
+int nau_get_mode(nau_ctx* ctx);
 /* Use an external CUDA stream (cudaStream_t), e.g. torch's current stream. NULL = own stream. */
 nau_status nau_set_stream(nau_ctx* ctx, void* stream);
 void* nau_get_stream(nau_ctx* ctx);

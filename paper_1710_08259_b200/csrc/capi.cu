@@ -7,6 +7,7 @@
 #include <string>
 
 #include "nau_internal.cuh"
+#include "sweep.cuh"
 
 using nau::FieldBuf;
 
@@ -71,6 +72,9 @@ void free_particles(nau_ctx* c) {
     dfree(c->d_perm);
     dfree(c->d_perm_tmp);
     dfree(c->d_okey);
+    dfree(c->d_xl);
+    dfree(c->d_aux);
+    dfree(c->d_p4);
 }
 
 void free_cells(nau_ctx* c) {
@@ -160,6 +164,13 @@ namespace nau {
 Geo make_geo(nau_ctx* c) {
     Geo g;
     g.dom = c->dom;
+    double ext_max = 0.0;
+    for (int a = 0; a < c->dom.dim; ++a) ext_max = std::fmax(ext_max, c->dom.ext[a]);
+    g.pre_abs = (float)(8.0 * ext_max * std::ldexp(1.0, -23));
+    for (int a = 0; a < 3; ++a) {
+        g.img[a] = AxisImg{c->dom.ext[a], 2.0 * c->dom.lo[a], 2.0 * c->dom.hi[a], c->dom.cs[a]};
+        g.lim[a] = a < c->dom.dim ? (float)(c->dom.cs[a] * 1.001) + g.pre_abs : 3.0e38f;
+    }
     g.n = c->n;
     g.x = c->fields[0].d;
     g.key = c->d_key;
@@ -168,6 +179,7 @@ Geo make_geo(nau_ctx* c) {
     g.cell_start = c->d_cell_start;
     g.cell_count = c->d_cell_count;
     g.nact = c->d_cell_start + c->dom.ncells;
+    g.p4 = c->d_p4;
     return g;
 }
 
@@ -330,7 +342,9 @@ nau_status nau_set_domain(nau_ctx* c, int dim, const int* min_cells, const int* 
 
 nau_status nau_set_particles(nau_ctx* c, long n, const double* pos_soa) {
     if (!c->has_domain) return fail(c, NAU_ERR_ARG, "nau_set_domain must precede nau_set_particles");
-    if (n < 0 || n >= 0x7fffffffL) return fail(c, NAU_ERR_ARG, "bad particle count");
+    if (n < 0 || n >= (1L << 25))  // sweep.cuh packs slot indices in 25 bits
+        return fail(c, NAU_ERR_ARG,
+                    "particle count must be below 2^25 per context (shard larger systems across GPUs)");
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     free_particles(c);
@@ -344,6 +358,9 @@ nau_status nau_set_particles(nau_ctx* c, long n, const double* pos_soa) {
     NAU_CUDA(dalloc(&c->d_perm, n));
     NAU_CUDA(dalloc(&c->d_perm_tmp, n));
     NAU_CUDA(dalloc(&c->d_okey, n));
+    NAU_CUDA(dalloc(&c->d_xl, n));
+    NAU_CUDA(dalloc(&c->d_aux, n));
+    NAU_CUDA(dalloc(&c->d_p4, n));
     if (n > 0) {
         k_iota<<<(int)((n + 255) / 256), 256, 0, c->stream>>>(n, c->d_orig);
         c->launches++;
@@ -600,7 +617,10 @@ nau_status nau_interact(nau_ctx* c, int op, int kf, int kdim, const nau_operand*
                                  cudaMemcpyDeviceToDevice, c->stream));
         out = of.alt;
     }
-    nau::launch_interact(c, op, kf, kdim, d_ops, nops, out, out_rows, out_cols, ar, acl);
+    if (c->mode == NAU_MODE_FAST && nau::fast_supports(op, ar, acl, dim))
+        nau::launch_interact_fast(c, op, kf, kdim, d_ops, out, ar);
+    else
+        nau::launch_interact(c, op, kf, kdim, d_ops, nops, out, out_rows, out_cols, ar, acl);
     if (alias) std::swap(of.d, of.alt);
     return NAU_OK;
 }
@@ -641,10 +661,24 @@ nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
         nau_status s = nau_build_cells(c);
         if (s != NAU_OK) return s;
     }
-    nau::launch_wcsph(c, p);
+    if (c->mode == NAU_MODE_FAST) {
+        nau::launch_wcsph_fast(c, p, c->d_aux);
+        nau::launch_symplectic(c, c->fields[p->f_v].d, c->fields[p->f_vdot].d,
+                               p->f_mask >= 0 ? c->fields[p->f_mask].d : nullptr, p->dt);
+    } else {
+        nau::launch_wcsph(c, p);
+    }
     c->dirty = true;
     return NAU_OK;
 }
+
+nau_status nau_set_mode(nau_ctx* c, int mode) {
+    if (mode != NAU_MODE_EXACT && mode != NAU_MODE_FAST) return fail(c, NAU_ERR_ARG, "unknown mode");
+    c->mode = mode;
+    return NAU_OK;
+}
+
+int nau_get_mode(nau_ctx* c) { return c->mode; }
 
 nau_status nau_reduce(nau_ctx* c, int kind, int id, double* out) {
     if (!field_ok(c, id) || kind < 0 || kind > 3) return fail(c, NAU_ERR_ARG, "bad reduce args");

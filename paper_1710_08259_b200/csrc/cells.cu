@@ -10,6 +10,7 @@
 //     5. k_reorder   one gather pass permuting every SoA field + orig/key/active
 // All passes are streaming (HBM-bound); see DESIGN.md for the per-particle bytes.
 #include "nau_internal.cuh"
+#include "sweep.cuh"
 
 namespace nau {
 
@@ -172,33 +173,49 @@ struct ReorderTable {
     double* dst[kMaxFields];
 };
 
-__global__ void k_reorder(long n, const int* perm, const int* orig, const int* key,
+// Also writes xl[s] = (float)(x - lo): global-origin fp32 coordinates, the
+// conservative pre-filter input of sweep.cuh / sweep_fast.cuh (NaN when inactive).
+__global__ void k_reorder(DomainDev d, long n, const int* perm, const int* orig, const int* key,
                           const uint8_t* active, int* orig_s, int* key_s, uint8_t* active_s,
-                          ReorderTable t) {
+                          float4* xl, double4* p4, ReorderTable t) {
     long s = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (s >= n) return;
     int k = perm[s];
+    const int kk = key[k];
     orig_s[s] = orig[k];
-    key_s[s] = key[k];
+    key_s[s] = kk;
     active_s[s] = active[k];
     for (int f = 0; f < t.nf; ++f) {
         const double* src = t.src[f];
         double* dst = t.dst[f];
         for (int c = 0; c < t.comps[f]; ++c) dst[c * n + s] = src[c * n + k];
     }
+    float4 p = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
+    double x[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < d.dim; ++a) x[a] = t.src[0][a * n + k];
+    if (kk < d.ncells) {
+        float v[3] = {0.f, 0.f, 0.f};
+        for (int a = 0; a < d.dim; ++a) v[a] = (float)(x[a] - d.lo[a]);
+        p = make_float4(v[0], v[1], v[2], 0.f);
+    }
+    xl[s] = p;
+    p4[s] = make_double4(x[0], x[1], x[2], 0.0);
 }
 
 template <int DIM>
-__global__ void k_neighbor_counts(Geo g, double radius, int* out) {
+__global__ void __launch_bounds__(kSweepThreads) k_neighbor_counts(Geo g, const float4* xl,
+                                                                   double radius, int* out) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= *g.nact) return;
+    const bool valid = k < *g.nact;
+    const int kk = valid ? k : 0;
     double xi[3] = {0.0, 0.0, 0.0};
-    for (int a = 0; a < DIM; ++a) xi[a] = g.x[a * g.n + k];
+    for (int a = 0; a < DIM; ++a) xi[a] = g.x[a * g.n + kk];
     int cnt = 0;
-    for_each_candidate<DIM>(g, k, xi, [&](int, const double* rel, int) {
+    sweep<DIM, false>(g, xl, k, valid, xi, (float)radius,
+               [&](int, const double* rel, int) {
         if (norm_rel<DIM>(rel) <= radius) ++cnt;
     });
-    out[g.orig[k]] = cnt;
+    if (valid) out[g.orig[k]] = cnt;
 }
 
 __global__ void k_unsort(long n, int comps, const int* orig, const double* src, double* dst) {
@@ -260,9 +277,9 @@ void launch_build_cells(nau_ctx* c) {
         t.dst[t.nf] = fb.alt;
         ++t.nf;
     }
-    k_reorder<<<blocks_for(n), kBlock, 0, c->stream>>>(n, c->d_perm, c->d_orig, c->d_key,
+    k_reorder<<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->d_perm, c->d_orig, c->d_key,
                                                        c->d_active, c->d_orig_s, c->d_key_s,
-                                                       c->d_active_s, t);
+                                                       c->d_active_s, c->d_xl, c->d_p4, t);
     c->launches += 3;
     std::swap(c->d_orig, c->d_orig_s);
     std::swap(c->d_key, c->d_key_s);
@@ -275,11 +292,12 @@ void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig) {
     cudaMemsetAsync(d_out_orig, 0, sizeof(int) * c->n, c->stream);
     if (c->n == 0) return;
     Geo g = make_geo(c);
-    int b = blocks_for(c->n, 128);
+    const int T = kSweepThreads;
+    int b = blocks_for(c->n, T);
     switch (c->dom.dim) {
-        case 1: k_neighbor_counts<1><<<b, 128, 0, c->stream>>>(g, radius, d_out_orig); break;
-        case 2: k_neighbor_counts<2><<<b, 128, 0, c->stream>>>(g, radius, d_out_orig); break;
-        default: k_neighbor_counts<3><<<b, 128, 0, c->stream>>>(g, radius, d_out_orig); break;
+        case 1: k_neighbor_counts<1><<<b, T, 0, c->stream>>>(g, c->d_xl, radius, d_out_orig); break;
+        case 2: k_neighbor_counts<2><<<b, T, 0, c->stream>>>(g, c->d_xl, radius, d_out_orig); break;
+        default: k_neighbor_counts<3><<<b, T, 0, c->stream>>>(g, c->d_xl, radius, d_out_orig); break;
     }
     c->launches++;
 }

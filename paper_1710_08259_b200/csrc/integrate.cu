@@ -13,13 +13,14 @@
 #include <cstring>
 
 #include "nau_internal.cuh"
+#include "sweep.cuh"
 
 namespace nau {
 
 namespace {
 
 constexpr int kBlock = 256;
-constexpr int kThreads = 128;
+constexpr int kThreads = kSweepThreads;
 inline int blocks_for(long n, int b = kBlock) { return (int)((n + b - 1) / b); }
 
 __global__ void k_euler(long n, int comps, const uint8_t* active, const int* orig, const double* x,
@@ -86,6 +87,7 @@ __global__ void k_symplectic(DomainDev d, long n, double* pos, double* v, const 
 
 struct WcsphArgs {
     Geo g;
+    const float4* xl;
     double mass, radius, rho0, B, gamma, visc, g_acc[3];
     int kdim;
     double* rho;
@@ -101,23 +103,26 @@ template <int DIM, int KF>
 __global__ void __launch_bounds__(kThreads) k_wcsph_density(const __grid_constant__ WcsphArgs a) {
     const Geo& g = a.g;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= *g.nact) return;
+    const bool valid = k < *g.nact;
+    const int kk = valid ? k : 0;
     const long n = g.n;
     double xi[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) xi[d] = g.x[d * n + k];
+    for (int d = 0; d < DIM; ++d) xi[d] = g.x[d * n + kk];
     const double radius = a.radius;
     const double h = 0.5 * radius;
     const double alpha = kernel_alpha<KF>(a.kdim, h);
     const double s_unit = a.mass / 1.0;  // m_j / rho_j with the uniform operand rho = 1
     double acc = 0.0;
-    for_each_candidate<DIM>(g, k, xi, [&](int, const double* rel, int) {
+    sweep<DIM, true>(g, a.xl, k, valid, xi, (float)radius,
+               [&](int, const double* rel, int) {
         const double dist = norm_rel<DIM>(rel);
         if (dist > radius) return;
         const double w = kernel_value<KF>(alpha, h, dist);
         if (w == 0.0) return;
         acc = acc + 1.0 * (s_unit * w);
     });
+    if (!valid) return;
     const double p = a.B * (pow(acc / a.rho0, a.gamma) - 1.0);
     if (!isfinite(acc) || !isfinite(p)) latch_error(a.err, 2, kMsgNan, g.orig[k]);
     a.rho[k] = acc;
@@ -130,28 +135,30 @@ template <int DIM, int KF>
 __global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_constant__ WcsphArgs a) {
     const Geo& g = a.g;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= *g.nact) return;
+    bool valid = k < *g.nact;
+    const int kk = valid ? k : 0;
     const long n = g.n;
     double xi[3] = {0.0, 0.0, 0.0}, v_i[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
-        xi[d] = g.x[d * n + k];
-        v_i[d] = a.v[d * n + k];
+        xi[d] = g.x[d * n + kk];
+        v_i[d] = a.v[d * n + kk];
     }
     const double radius = a.radius;
     const double h = 0.5 * radius;
     const double alpha = kernel_alpha<KF>(a.kdim, h);
     const double m = a.mass;
-    const double rho_i = a.rho[k];
-    const double p_i = a.p[k];
-    const int my_orig = g.orig[k];
-    if (rho_i == 0.0) {
+    const double rho_i = a.rho[kk];
+    const double p_i = a.p[kk];
+    const int my_orig = g.orig[kk];
+    if (valid && rho_i == 0.0) {
         latch_error(a.err, 1, kMsgZeroDensity, my_orig);
-        return;
+        valid = false;
     }
     const double pr_i = p_i / (rho_i * rho_i);
     double G[3] = {0.0, 0.0, 0.0}, A[3] = {0.0, 0.0, 0.0};
-    for_each_candidate<DIM>(g, k, xi, [&](int j, const double* rel, int mask) {
+    sweep<DIM, true>(g, a.xl, k, valid, xi, (float)radius,
+               [&](int j, const double* rel, int mask) {
         const double dist = norm_rel<DIM>(rel);
         if (dist > radius) return;
         if (dist <= 0.0) {  // G11 skips silently; sph_A warns (interactions.cpp:32-38)
@@ -177,6 +184,7 @@ __global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_consta
 #pragma unroll
         for (int d = 0; d < DIM; ++d) A[d] = A[d] + (rel[d] * sc) * sa;
     });
+    if (!valid) return;
     const double s1 = -1.0 / rho_i;
     bool bad = false;
 #pragma unroll
@@ -276,6 +284,7 @@ void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p) {
     if (c->n == 0) return;
     WcsphArgs a;
     a.g = make_geo(c);
+    a.xl = c->d_xl;
     a.mass = p->mass;
     a.radius = p->radius;
     a.rho0 = p->rho0;

@@ -13,15 +13,17 @@
 #include <cstring>
 
 #include "nau_internal.cuh"
+#include "sweep.cuh"
 
 namespace nau {
 
 namespace {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = kSweepThreads;
 
 struct SphArgs {
     Geo g;
+    const float4* xl;
     Opd A, m, rho, R;
     double* out;
     int arows, acols;
@@ -33,16 +35,17 @@ template <int DIM, int OP, int KF, int AC>
 __global__ void __launch_bounds__(kThreads) k_sph(const __grid_constant__ SphArgs a) {
     const Geo& g = a.g;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= *g.nact) return;
+    bool valid = k < *g.nact;
     const long n = g.n;
+    const int kk = valid ? k : 0;
     double xi[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) xi[d] = g.x[d * n + k];
+    for (int d = 0; d < DIM; ++d) xi[d] = g.x[d * n + kk];
     // sph_context (interactions.cpp:22-27)
-    const double radius = a.R.at(0, k, n);
-    if (!(radius > 0.0)) {
+    const double radius = a.R.at(0, kk, n);
+    if (valid && !(radius > 0.0)) {
         latch_error(a.err, 1, kMsgRadius, g.orig[k]);
-        return;
+        valid = false;
     }
     const double h = 0.5 * radius;
     const double alpha = kernel_alpha<KF>(a.kdim, h);
@@ -51,21 +54,22 @@ __global__ void __launch_bounds__(kThreads) k_sph(const __grid_constant__ SphArg
                                       : ((OP == NAU_OP_SPH_D00 || OP == NAU_OP_SPH_A) ? DIM : 1);
     double a_i[9];
 #pragma unroll
-    for (int c = 0; c < 9; ++c) a_i[c] = (c < ac) ? a.A.at(c, k, n) : 0.0;
+    for (int c = 0; c < 9; ++c) a_i[c] = (c < ac) ? a.A.at(c, kk, n) : 0.0;
     double rho_i = 1.0;
     if (OP == NAU_OP_SPH_G11 || OP == NAU_OP_SPH_A) {
-        rho_i = a.rho.at(0, k, n);
-        if (rho_i == 0.0) {
+        rho_i = a.rho.at(0, kk, n);
+        if (valid && rho_i == 0.0) {
             latch_error(a.err, 1, kMsgZeroDensity, g.orig[k]);
-            return;
+            valid = false;
         }
     }
     double acc[9];
 #pragma unroll
     for (int c = 0; c < 9; ++c) acc[c] = 0.0;
-    const int my_orig = g.orig[k];
+    const int my_orig = g.orig[kk];
 
-    for_each_candidate<DIM>(g, k, xi, [&](int j, const double* rel, int mask) {
+    sweep<DIM, true>(g, a.xl, k, valid, xi, (float)radius,
+               [&](int j, const double* rel, int mask) {
         const double dist = norm_rel<DIM>(rel);
         if (OP == NAU_OP_SPH_S) {  // interactions.cpp:40-58
             if (dist > radius) return;
@@ -154,6 +158,7 @@ __global__ void __launch_bounds__(kThreads) k_sph(const __grid_constant__ SphArg
 #pragma unroll
         for (int d = 0; d < DIM; ++d) acc[d] = rho_i * acc[d];
     }
+    if (!valid) return;
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
         if (c < oc) {
@@ -166,6 +171,7 @@ __global__ void __launch_bounds__(kThreads) k_sph(const __grid_constant__ SphArg
 // ---- DEM contact sums: dem_sum (interactions.cpp:152-193) ----
 struct DemArgs {
     Geo g;
+    const float4* xl;
     Opd v, R, P, Q, m, cf, Rs;  // P = E (Hertz) | kn (LSD); Q = nu (Hertz) | en (LSD)
     double zeta_uniform;        // LSD damping ratio from a uniform en (host libm), else NaN
     double* out;
@@ -176,19 +182,20 @@ template <int DIM, int OP>
 __global__ void __launch_bounds__(kThreads) k_dem(const __grid_constant__ DemArgs a) {
     const Geo& g = a.g;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= *g.nact) return;
+    const bool valid = k < *g.nact;
+    const int kk = valid ? k : 0;
     const long n = g.n;
     constexpr bool kImagesOnly = OP == NAU_OP_DEM_BOUNDARY;
     constexpr bool kLsd = OP == NAU_OP_DEM_LSD;
     double xi[3] = {0.0, 0.0, 0.0}, v_i[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
-        xi[d] = g.x[d * n + k];
-        v_i[d] = a.v.at(d, k, n);
+        xi[d] = g.x[d * n + kk];
+        v_i[d] = a.v.at(d, kk, n);
     }
-    const double radius = a.Rs.at(0, k, n);
-    const double Ri = a.R.at(0, k, n), Pi = a.P.at(0, k, n), Qi = a.Q.at(0, k, n);
-    const double mi = a.m.at(0, k, n), fr = a.cf.at(0, k, n);
+    const double radius = a.Rs.at(0, kk, n);
+    const double Ri = a.R.at(0, kk, n), Pi = a.P.at(0, kk, n), Qi = a.Q.at(0, kk, n);
+    const double mi = a.m.at(0, kk, n), fr = a.cf.at(0, kk, n);
     double zeta = 0.0;
     if (kLsd) {
         if (a.zeta_uniform == a.zeta_uniform) {
@@ -198,9 +205,10 @@ __global__ void __launch_bounds__(kThreads) k_dem(const __grid_constant__ DemArg
             zeta = -le / sqrt(kPi * kPi + le * le);
         }
     }
-    const int my_orig = g.orig[k];
+    const int my_orig = g.orig[kk];
     double acc[3] = {0.0, 0.0, 0.0};
-    for_each_candidate<DIM>(g, k, xi, [&](int j, const double* rel, int mask) {
+    sweep<DIM, true>(g, a.xl, k, valid, xi, (float)radius,
+               [&](int j, const double* rel, int mask) {
         const double dist = norm_rel<DIM>(rel);
         if (dist > radius) return;
         if (kImagesOnly && mask == 0) return;
@@ -263,6 +271,7 @@ __global__ void __launch_bounds__(kThreads) k_dem(const __grid_constant__ DemArg
 #pragma unroll
         for (int d = 0; d < DIM; ++d) acc[d] = acc[d] + f[d];
     });
+    if (!valid) return;
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
         double r = kImagesOnly ? acc[d] : acc[d] / mi;
@@ -399,6 +408,7 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
     if (op <= NAU_OP_SPH_A) {
         SphArgs a;
         a.g = make_geo(c);
+        a.xl = c->d_xl;
         a.A = ops[0];
         a.m = ops[1];
         a.rho = ops[2];
@@ -436,6 +446,7 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
     } else {
         DemArgs a;
         a.g = make_geo(c);
+        a.xl = c->d_xl;
         a.v = ops[0];
         a.R = ops[1];
         a.P = ops[2];

@@ -61,9 +61,19 @@ struct Opd {
     }
 };
 
+// Per-axis image constants (particle_system.hpp:113-119): 2*lo and 2*hi are
+// exact scalings, so precomputing them keeps the reference's rounding.
+struct AxisImg {
+    double ext, twolo, twohi, cs;
+};
+
 // Geometry bundle handed to every neighbour kernel.
 struct Geo {
     DomainDev dom;
+    AxisImg img[3];
+    const double4* p4;  // positions packed (x, y, z, 0) per slot, for gathers
+    float lim[3];    // fp32 pre-filter per-axis limit: cell size * (1 + 1e-3) + pre_abs
+    float pre_abs;   // absolute fp32 error bound of u = x - lo differences (8 ulp of extent)
     long n;
     const double* x;  // pos component 0..dim-1 (x + a*n)
     const int* key;
@@ -312,6 +322,10 @@ struct nau_ctx {
     int* d_perm = nullptr;
     int* d_perm_tmp = nullptr;
     int* d_okey = nullptr;
+    float4* d_xl = nullptr;  // fp32 global-origin coordinates (sweep pre-filters)
+    double4* d_aux = nullptr;  // per-particle scratch (fast WCSPH: v and p / rho^2 packed)
+    double4* d_p4 = nullptr;  // packed positions (written by the reorder pass)
+    int mode = NAU_MODE_EXACT;
     int* d_cell_start = nullptr;  // ncells + 2
     int* d_cell_count = nullptr;  // ncells + 1
     int* d_cursor = nullptr;      // ncells + 1
@@ -355,4 +369,9 @@ void launch_euler(nau_ctx* c, const double* x, const double* xdot, double dt, do
 void launch_symplectic(nau_ctx* c, double* v, const double* vdot, const double* mask, double dt);
 void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p);
 void launch_reduce(nau_ctx* c, int kind, const double* f, int comps, double* h_out);
+// fast.cu
+bool fast_supports(int op, int a_rows, int a_cols, int dim);
+void launch_interact_fast(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, double* out,
+                          int a_rows);
+void launch_wcsph_fast(nau_ctx* c, const nau_wcsph_params* p, double4* vp);
 }  // namespace nau

@@ -1,0 +1,233 @@
+// sweep.cuh — warp-cooperative neighbour sweep with a deferred pair queue.
+//
+// Same candidate set as the reference's ParticleSystem::for_each_neighbor
+// (particle_system.hpp:59-138), restructured for SIMT efficiency
+// (profiles/r1_v0_ncu_full_cfg2.md: the one-pass version ran 18 of 32 lanes per
+// instruction and the pair arithmetic of an accepted pair at ~15% lane
+// occupancy, because only ~1 in 6 candidates lies inside the support):
+//
+//   phase A (scan)   each lane (= one particle) walks ITS candidate sequence —
+//                    stencil options, each option's cell range in slot order —
+//                    testing candidates with a conservative fp32 pre-filter on the
+//                    global-origin coordinates u = x - lo (float4 xl[], written by
+//                    the reorder pass). Survivors go to the lane's FIFO in shared
+//                    memory as (slot j | image code << 25).
+//   phase B (drain)  when a FIFO could overflow on the next chunk, or all lanes
+//                    are done, the warp drains the FIFOs in lockstep: lane L takes
+//                    its q-th entry, recomputes image and rel in fp64 exactly as the
+//                    reference (per-axis |rel_a| > cell_size rejection included) and
+//                    calls fn(j, rel, mirror_mask) — the operator's pair rule.
+//
+// Option order. ORDERED = true walks the options in the reference's odometer
+// order (axis 0 fastest): with FIFO order == candidate order every accumulator
+// sums exactly as interact() does (bitwise EXACT mode). ORDERED = false (FAST
+// mode, and the order-free neighbour count) visits option i and its point
+// reflection N-1-i back to back: which cells a particle accepts from depends on
+// where it sits in its cell, so in odometer order the lanes' FIFOs fill at very
+// different rates mid-sweep and a drain runs at mean/max fill occupancy (53% on
+// cfg2, profiles/r1_v3_*); opposite cells compensate each other.
+// The pre-filter only ever passes a superset of the exact test (margin 1e-3 R
+// plus 8 ulp of the extent; NaN passes).
+#pragma once
+
+#include "nau_internal.cuh"
+
+namespace nau {
+
+constexpr int kQueue = 64;          // FIFO depth per lane (8 KB of shared memory per warp)
+constexpr int kChunk = 16;          // max candidates scanned between warp votes
+constexpr int kSweepThreads = 128;  // 4 warps, 32 KB shared memory per CTA
+constexpr int kSlotBits = 25;       // FIFO entry = slot | image code << 25 (n < 2^25 per context)
+
+struct SweepSmem {
+    uint32_t e[kQueue * 32];
+};
+
+// Per-axis image code: 0 direct, 1 direct + extent, 2 direct - extent,
+// 3 mirror across the low wall, 4 mirror across the high wall. Branch-free:
+// img = (+/-xj) + off reproduces xj + shift and 2*lo - xj / 2*hi - xj exactly.
+__device__ __forceinline__ double image_of(const AxisImg& ax, double xj, int c) {
+    const double off = c == 0 ? 0.0 : (c == 1 ? ax.ext : (c == 2 ? -ax.ext : (c == 3 ? ax.twolo : ax.twohi)));
+    const double xs = c >= 3 ? -xj : xj;
+    return xs + off;
+}
+
+template <int DIM>
+__device__ __forceinline__ void decode_cell(const DomainDev& d, int key, int* ci) {
+    ci[0] = key % d.cells[0];
+    ci[1] = DIM > 1 ? (key / d.cells[0]) % d.cells[1] : 0;
+    ci[2] = DIM > 2 ? key / (d.cells[0] * d.cells[1]) : 0;
+}
+
+// Option `o` of axis a -> cell, image code, pre-filter transform in global-origin
+// coordinates u = x - lo: u_img = sg * u_j + bs.
+__device__ __forceinline__ void option_of(const DomainDev& d, int a, int ci, const AxisOpts& ao,
+                                          int o, int& cell, int& icode, float& sg, float& bs) {
+    const int n = d.cells[a];
+    const float ext = (float)d.ext[a];
+    if (o < ao.ndir) {
+        int c = ci + ao.lo_off + o;
+        icode = 0;
+        bs = 0.0f;
+        if (c < 0) {
+            c += n;
+            icode = 2;  // shift = -extent
+            bs = -ext;
+        } else if (c >= n) {
+            c -= n;
+            icode = 1;  // shift = +extent
+            bs = ext;
+        }
+        cell = c;
+        sg = 1.0f;
+    } else if (o == ao.ndir && ci == 0) {
+        cell = 0;
+        icode = 3;  // 2 lo - x  ->  -u
+        sg = -1.0f;
+        bs = 0.0f;
+    } else {
+        cell = n - 1;
+        icode = 4;  // 2 hi - x  ->  2 ext - u
+        sg = -1.0f;
+        bs = 2.0f * ext;
+    }
+}
+
+// The sweep. Must be called by all 32 lanes of a warp (valid = false for lanes
+// without a particle). `pre_r` is the pre-filter radius (>= the operator's
+// acceptance radius).
+template <int DIM, bool ORDERED, class Fn>
+__device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ xl4, int k,
+                                      bool valid, const double* xi, float pre_r, Fn&& fn) {
+    __shared__ SweepSmem smem[kSweepThreads / 32];
+    const DomainDev& d = g.dom;
+    const int lane = threadIdx.x & 31;
+    uint32_t* qe = smem[threadIdx.x >> 5].e + lane;
+    int ci[3] = {0, 0, 0};
+    AxisOpts ao[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ao[a] = AxisOpts{0, 1, 1};
+    float xli[3] = {0.f, 0.f, 0.f};
+    bool done = !valid;
+    if (valid) {
+        decode_cell<DIM>(d, g.key[k], ci);
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) ao[a] = axis_opts(d, a, ci[a]);
+        const float4 p = xl4[k];
+        xli[0] = p.x;
+        xli[1] = p.y;
+        xli[2] = p.z;
+    }
+    const float rl = pre_r * 1.001f + g.pre_abs;
+    const float r2lim = rl * rl;
+    const int n01 = ao[0].cnt * (DIM > 1 ? ao[1].cnt : 1);
+    const int ncombo = n01 * (DIM > 2 ? ao[2].cnt : 1);
+    int idx = -1;  // position in the option sequence
+    int t = 0, e = 0;
+    uint32_t icode = 0;  // (c0 + 5 c1 + 25 c2) << kSlotBits
+    float sg[3] = {1.f, 1.f, 1.f}, bq[3] = {0.f, 0.f, 0.f};  // rel_f = sg * u_j + bq
+    int fill = 0;
+
+    auto advance = [&]() {
+        while (t >= e) {
+            if (++idx == ncombo) {
+                done = true;
+                return;
+            }
+            const int combo = ORDERED ? idx : ((idx & 1) ? ncombo - 1 - (idx >> 1) : (idx >> 1));
+            const int o0 = combo % ao[0].cnt;
+            const int o1 = DIM > 1 ? (combo / ao[0].cnt) % ao[1].cnt : 0;
+            const int o2 = DIM > 2 ? combo / n01 : 0;
+            int cell, ic;
+            float bs;
+            option_of(d, 0, ci[0], ao[0], o0, cell, ic, sg[0], bs);
+            int flat = cell;
+            int code = ic;
+            bq[0] = bs - xli[0];
+            if (DIM > 1) {
+                option_of(d, 1, ci[1], ao[1], o1, cell, ic, sg[1], bs);
+                flat += d.cells[0] * cell;
+                code += 5 * ic;
+                bq[1] = bs - xli[1];
+            }
+            if (DIM > 2) {
+                option_of(d, 2, ci[2], ao[2], o2, cell, ic, sg[2], bs);
+                flat += d.cells[0] * d.cells[1] * cell;
+                code += 25 * ic;
+                bq[2] = bs - xli[2];
+            }
+            icode = (uint32_t)code << kSlotBits;
+            t = g.cell_start[flat];
+            e = t + g.cell_count[flat];
+        }
+    };
+    if (!done) advance();
+
+    auto test = [&](const float4 p) {
+        const float r0 = fmaf(sg[0], p.x, bq[0]);
+        bool rej = fabsf(r0) > g.lim[0];
+        float r2 = r0 * r0;
+        if (DIM > 1) {
+            const float r1 = fmaf(sg[1], p.y, bq[1]);
+            rej |= fabsf(r1) > g.lim[1];
+            r2 = fmaf(r1, r1, r2);
+        }
+        if (DIM > 2) {
+            const float r3 = fmaf(sg[2], p.z, bq[2]);
+            rej |= fabsf(r3) > g.lim[2];
+            r2 = fmaf(r3, r3, r2);
+        }
+        return !(rej || r2 > r2lim);
+    };
+
+    while (true) {
+        if (!done) {
+            const int stop = min(e, t + kChunk);
+            // four independent loads in flight per lane
+            for (; t + 4 <= stop; t += 4) {
+                const float4 p0 = xl4[t], p1 = xl4[t + 1], p2 = xl4[t + 2], p3 = xl4[t + 3];
+                const bool a0 = test(p0), a1 = test(p1), a2 = test(p2), a3 = test(p3);
+                if (a0) qe[(fill++) * 32] = (uint32_t)t | icode;
+                if (a1) qe[(fill++) * 32] = (uint32_t)(t + 1) | icode;
+                if (a2) qe[(fill++) * 32] = (uint32_t)(t + 2) | icode;
+                if (a3) qe[(fill++) * 32] = (uint32_t)(t + 3) | icode;
+            }
+            for (; t < stop; ++t)
+                if (test(xl4[t])) qe[(fill++) * 32] = (uint32_t)t | icode;
+            if (t >= e) advance();
+        }
+        const bool need = __any_sync(0xffffffffu, fill > kQueue - kChunk);
+        const bool live = __any_sync(0xffffffffu, !done);
+        if (need || !live) {
+            __syncwarp();
+            const int maxf = __reduce_max_sync(0xffffffffu, fill);
+            for (int s = 0; s < maxf; ++s) {
+                if (s < fill) {
+                    const uint32_t ent = qe[s * 32];
+                    const int j = (int)(ent & ((1u << kSlotBits) - 1));
+                    const int c = (int)(ent >> kSlotBits);
+                    const int cc[3] = {c % 5, (c / 5) % 5, c / 25};
+                    double rel[3] = {0.0, 0.0, 0.0};
+                    bool ok = true;
+                    int mask = 0;
+                    const double4 pj = g.p4[j];  // one 32-byte sector per pair
+                    const double xj[3] = {pj.x, pj.y, pj.z};
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) {
+                        const int ca = cc[a];
+                        const double r = image_of(g.img[a], xj[a], ca) - xi[a];
+                        ok &= !(fabs(r) > g.img[a].cs);
+                        rel[a] = r;
+                        mask |= (ca >= 3) << a;
+                    }
+                    if (ok) fn(j, rel, mask);
+                }
+            }
+            fill = 0;
+            __syncwarp();
+        }
+        if (!live) break;
+    }
+}
+
+}  // namespace nau

@@ -23,6 +23,7 @@ PERIODIC, SYMMETRIC, CUTOFF = 0, 1, 2
 OPS = {"sph_S": 0, "sph_D00": 1, "sph_G11": 2, "sph_L0": 3, "sph_A": 4, "dem_l": 5,
        "dem_boundary_force": 6, "nbody_gravity": 7, "dem_lsd": 8}
 K_WENDLAND, K_CUBIC = 0, 1
+MODE_EXACT, MODE_FAST = 0, 1
 STATUS = {0: "ok", 1: "runtime error", 2: "runtime NaN", 3: "CUDA error", 4: "argument error",
           5: "communication error"}
 
@@ -35,7 +36,7 @@ EXPORTS = [
     "nau_build_cells", "nau_cells_dirty", "nau_rebuild_count", "nau_warning_count", "nau_ncells",
     "nau_cell_tables", "nau_neighbor_counts", "nau_interact", "nau_euler", "nau_symplectic_step",
     "nau_wcsph_step", "nau_reduce", "nau_sync", "nau_last_error", "nau_profile_enable",
-    "nau_profile_ms", "nau_launch_count", "nau_fp64_peak_tflops",
+    "nau_profile_ms", "nau_launch_count", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
 ]
 
 
@@ -116,6 +117,8 @@ def load():
         "nau_profile_ms": (d, [vp, i, C.POINTER(l)]),
         "nau_launch_count": (l, [vp]),
         "nau_fp64_peak_tflops": (d, [i]),
+        "nau_set_mode": (i, [vp, i]),
+        "nau_get_mode": (i, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -194,6 +197,14 @@ class Context:
             raise NauError(st, msg, bad.value)
 
     # ---- setup ----
+    def set_mode(self, fast: bool):
+        """EXACT (reference order, bitwise) or FAST (warp per particle, tolerance)."""
+        self._check(self.L.nau_set_mode(self.h, MODE_FAST if fast else MODE_EXACT))
+
+    @property
+    def fast(self):
+        return self.L.nau_get_mode(self.h) == MODE_FAST
+
     def set_stream(self, stream_ptr):
         self._check(self.L.nau_set_stream(self.h, C.c_void_p(stream_ptr)))
 
@@ -240,7 +251,9 @@ class Context:
         return f.comps
 
     def upload(self, f, values):
-        a = np.ascontiguousarray(np.asarray(values, dtype=np.float64).reshape(-1, self.n))
+        a = np.ascontiguousarray(np.atleast_2d(np.asarray(values, dtype=np.float64)))
+        if a.shape[-1] != self.n or a.shape[0] != self._comps(f):
+            a = np.ascontiguousarray(a.reshape(self._comps(f), self.n))
         self._check(self.L.nau_upload(self.h, self._fid(f), _p(a), self.n))
 
     def upload_ptr(self, f, host_ptr):

@@ -275,3 +275,64 @@ def test_euler_and_reduce(ctx):
     assert ctx.reduce("fmax", "A")[0] == spec["fields"]["A"].max()
     nrm = np.sqrt((V * V).sum(axis=0))
     assert ctx.reduce("fmin", "V")[0] == pytest.approx(nrm.min(), rel=1e-15)
+
+
+# ---------------------------------------------------------------- FAST mode ----
+SPH_NAMES = {"sph_S", "sph_D00", "sph_G11", "sph_L0", "sph_A"}
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fast_mode_matches_exact(ctx, seed):
+    """FAST mode (warp per particle, FMA/rsqrt, tree sums) vs EXACT on the same inputs."""
+    rng = np.random.default_rng(300 + seed)
+    spec = cases.random_spec(rng, n=int(rng.integers(300, 3000)))
+    cases.gpu_context(spec, ctx)
+    for entry in cases.op_list(spec["dim"]):
+        if entry[0] not in SPH_NAMES:
+            continue
+        ctx.set_mode(False)
+        exact = cases.gpu_eval(spec, ctx, entry)
+        ctx.set_mode(True)
+        fast = cases.gpu_eval(spec, ctx, entry)
+        ctx.set_mode(False)
+        assert rel_err(fast, exact) <= 1e-12, (entry[0], entry[2], rel_err(fast, exact))
+
+
+def test_fast_mode_microbench_full_size(ctx):
+    sc = scenes.sph_microbench()
+    prm = sc.params
+    ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+    ctx.set_particles(sc.pos)
+    ctx.add_field("A", 1, 1, sc.fields["A"])
+    for f, r in (("rho", 1), ("G", 3), ("L", 1)):
+        ctx.add_field(f, r, 1, 0.0)
+    ctx.boundary_shift()
+    out = {}
+    for fast in (False, True):
+        ctx.set_mode(fast)
+        ctx.interact("sph_S", [1.0, prm["mass"], 1.0, prm["radius"]], "rho", kernel="Wc33220")
+        ctx.interact("sph_G11", ["A", prm["mass"], "rho", prm["radius"]], "G", kernel="Wc33220")
+        ctx.interact("sph_L0", ["A", prm["mass"], "rho", prm["radius"]], "L", kernel="Wc33220")
+        out[fast] = {k: ctx.download(k) for k in ("rho", "G", "L")}
+    ctx.set_mode(False)
+    for k in ("rho", "G", "L"):
+        assert rel_err(out[True][k], out[False][k]) <= TOL_STEP, k
+
+
+def test_fast_mode_dam_break_vs_port(ctx):
+    """cfg0 deck in FAST mode: 1 step within 1e-10, 10 steps within 1e-6 of the oracle."""
+    sc = scenes.dam_break(2)
+    prm = sc.params
+    p = _gpu_dam(ctx, sc)
+    ctx.set_mode(True)
+    ps, st = deck_oracle.make_system(sc)
+    for s in range(1, 11):
+        ctx.wcsph_step(p)
+        deck_oracle.step(ps, st, prm)
+        if s in (1, 10):
+            tol = TOL_STEP if s == 1 else TOL_10
+            assert rel_err(ctx.download("r"), ps.pos) <= tol
+            for k in ("rho", "p", "v"):
+                assert rel_err(ctx.download(k), st[k]) <= tol, (s, k)
+    ctx.set_mode(False)
+    np.testing.assert_array_equal(ctx.active(), ps.active)
