@@ -163,21 +163,70 @@ __device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ x
     };
     if (!done) advance();
 
+    // When the acceptance radius is <= every cell size, |rel_a| <= |rel| <= R makes
+    // the per-axis cell test redundant for accepted pairs (kernel-uniform flag).
+    // (min_cs is rounded down; the 1e-6 factor covers the rounding of pre_r.)
+    const bool axis_implied = pre_r * 1.000001f <= g.min_cs;
     auto test = [&](const float4 p) {
         const float r0 = fmaf(sg[0], p.x, bq[0]);
-        bool rej = fabsf(r0) > g.lim[0];
+        bool rej = !axis_implied && fabsf(r0) > g.lim[0];
         float r2 = r0 * r0;
         if (DIM > 1) {
             const float r1 = fmaf(sg[1], p.y, bq[1]);
-            rej |= fabsf(r1) > g.lim[1];
+            rej |= !axis_implied && fabsf(r1) > g.lim[1];
             r2 = fmaf(r1, r1, r2);
         }
         if (DIM > 2) {
             const float r3 = fmaf(sg[2], p.z, bq[2]);
-            rej |= fabsf(r3) > g.lim[2];
+            rej |= !axis_implied && fabsf(r3) > g.lim[2];
             r2 = fmaf(r3, r3, r2);
         }
         return !(rej || r2 > r2lim);
+    };
+
+    // Ring FIFO per lane: entries [head, head + fill) (mod kQueue), oldest first.
+    int head = 0;
+    auto push = [&](uint32_t ent) {
+        qe[((head + fill) & (kQueue - 1)) * 32] = ent;
+        ++fill;
+    };
+    // Process the `steps` oldest entries of every lane (fewer if a lane has fewer).
+    auto drain = [&](int steps) {
+        __syncwarp();
+        for (int s = 0; s < steps; ++s) {
+            if (s < fill) {
+                const uint32_t ent = qe[((head + s) & (kQueue - 1)) * 32];
+                const int j = (int)(ent & ((1u << kSlotBits) - 1));
+                const int c = (int)(ent >> kSlotBits);
+                const double4 pj = g.p4[j];  // one 32-byte sector per pair
+                const double xj[3] = {pj.x, pj.y, pj.z};
+                double rel[3] = {0.0, 0.0, 0.0};
+                bool ok = true;
+                int mask = 0;
+                if (c == 0) {  // direct image in every axis: img = xj + 0.0
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) {
+                        rel[a] = (xj[a] + 0.0) - xi[a];
+                        ok &= axis_implied || !(fabs(rel[a]) > g.img[a].cs);
+                    }
+                } else {
+                    const int cc[3] = {c % 5, (c / 5) % 5, c / 25};
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) {
+                        const int ca = cc[a];
+                        const double r = image_of(g.img[a], xj[a], ca) - xi[a];
+                        ok &= axis_implied || !(fabs(r) > g.img[a].cs);
+                        rel[a] = r;
+                        mask |= (ca >= 3) << a;
+                    }
+                }
+                if (ok) fn(j, rel, mask);
+            }
+        }
+        const int took = min(fill, steps);
+        head = (head + took) & (kQueue - 1);
+        fill -= took;
+        __syncwarp();
     };
 
     while (true) {
@@ -187,46 +236,22 @@ __device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ x
             for (; t + 4 <= stop; t += 4) {
                 const float4 p0 = xl4[t], p1 = xl4[t + 1], p2 = xl4[t + 2], p3 = xl4[t + 3];
                 const bool a0 = test(p0), a1 = test(p1), a2 = test(p2), a3 = test(p3);
-                if (a0) qe[(fill++) * 32] = (uint32_t)t | icode;
-                if (a1) qe[(fill++) * 32] = (uint32_t)(t + 1) | icode;
-                if (a2) qe[(fill++) * 32] = (uint32_t)(t + 2) | icode;
-                if (a3) qe[(fill++) * 32] = (uint32_t)(t + 3) | icode;
+                if (a0) push((uint32_t)t | icode);
+                if (a1) push((uint32_t)(t + 1) | icode);
+                if (a2) push((uint32_t)(t + 2) | icode);
+                if (a3) push((uint32_t)(t + 3) | icode);
             }
             for (; t < stop; ++t)
-                if (test(xl4[t])) qe[(fill++) * 32] = (uint32_t)t | icode;
+                if (test(xl4[t])) push((uint32_t)t | icode);
             if (t >= e) advance();
         }
-        const bool need = __any_sync(0xffffffffu, fill > kQueue - kChunk);
-        const bool live = __any_sync(0xffffffffu, !done);
-        if (need || !live) {
-            __syncwarp();
-            const int maxf = __reduce_max_sync(0xffffffffu, fill);
-            for (int s = 0; s < maxf; ++s) {
-                if (s < fill) {
-                    const uint32_t ent = qe[s * 32];
-                    const int j = (int)(ent & ((1u << kSlotBits) - 1));
-                    const int c = (int)(ent >> kSlotBits);
-                    const int cc[3] = {c % 5, (c / 5) % 5, c / 25};
-                    double rel[3] = {0.0, 0.0, 0.0};
-                    bool ok = true;
-                    int mask = 0;
-                    const double4 pj = g.p4[j];  // one 32-byte sector per pair
-                    const double xj[3] = {pj.x, pj.y, pj.z};
-#pragma unroll
-                    for (int a = 0; a < DIM; ++a) {
-                        const int ca = cc[a];
-                        const double r = image_of(g.img[a], xj[a], ca) - xi[a];
-                        ok &= !(fabs(r) > g.img[a].cs);
-                        rel[a] = r;
-                        mask |= (ca >= 3) << a;
-                    }
-                    if (ok) fn(j, rel, mask);
-                }
-            }
-            fill = 0;
-            __syncwarp();
+        // Partial drains of the oldest kChunk entries keep every drain step busy for
+        // all lanes holding >= kChunk entries (mean/max-fill occupancy otherwise).
+        if (__any_sync(0xffffffffu, fill > kQueue - kChunk)) drain(kChunk);
+        if (!__any_sync(0xffffffffu, !done)) {
+            drain(__reduce_max_sync(0xffffffffu, fill));
+            break;
         }
-        if (!live) break;
     }
 }
 
