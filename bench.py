@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the bounded reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slab", action="store_true",
+                    help="cfg0/cfg2: run the slab-decomposed path even on one GPU")
     ap.add_argument("--mode", default="fast", choices=["fast", "exact"],
                     help="fast: warp-per-particle sums (1e-10 tolerance); exact: reference order, bitwise")
     return ap.parse_args()
@@ -346,7 +348,92 @@ class DamBreak(Workload):
                 "neighbours_per_particle": round(self.nbr_per_particle, 2)}
 
 
-def make_workload(cfg):
+class DamBreakSlab(DamBreak):
+    """cfg2/cfg0 slab-decomposed along x over the ranks (paper_1710_08259_b200/slab.py):
+    each rank owns whole x-cell planes (balanced on particle counts) plus two ghost
+    planes per face; migration + ghost refresh over NCCL every step."""
+
+    FIELDS = ["rho", "p", "v", "vdot", "mask"]
+
+    def __init__(self, dim, dist):
+        super().__init__(dim)
+        self.dist = dist
+
+    def setup(self, ctx):
+        import torch
+        from paper_1710_08259_b200 import nau, slab
+        sc, prm = self.sc, self.sc.params
+        periodic = sc.kinds[0] == 0
+        ncx = sc.max_cells[0] - sc.min_cells[0]
+        lo, cs = sc.min_cells[0] * sc.cell_size[0], sc.cell_size[0]
+        cx = slab.cell_x_of(sc.pos[0], lo, cs, ncx, periodic)
+        world, rank = self.dist.world, self.dist.rank
+        self.bounds = slab.balanced_bounds(cx, ncx, world)
+        rows = slab.initial_rows(sc, self.FIELDS, self.bounds, rank, ncx, periodic)
+        d = sc.dim
+        ctx.set_domain(sc.dim, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+        ctx.set_particles(np.ascontiguousarray(rows[:, :d].T))
+        col = d
+        for k in self.FIELDS + ["gid", "ghost"]:
+            w = d if k in ("v", "vdot") else 1
+            ctx.add_field(k, w, 1, np.ascontiguousarray(rows[:, col:col + w].T))
+            col += w
+        ctx.boundary_shift()
+        ctx.build_cells()
+        p = nau.WcsphParams()
+        p.kernel_family, p.kernel_dim = nau.K_WENDLAND, sc.dim
+        p.mass, p.radius, p.rho0, p.B = prm["mass"], prm["radius"], prm["rho0"], prm["B"]
+        p.gamma, p.visc, p.dt = prm["gamma"], prm["visc"], prm["dt"]
+        for a in range(sc.dim):
+            p.g[a] = prm["g"][a]
+        f = ctx.fields
+        p.f_rho, p.f_p, p.f_v, p.f_vdot, p.f_mask = (f["rho"].id, f["p"].id, f["v"].id,
+                                                     f["vdot"].id, f["mask"].id)
+        self.p = p
+        self.backend = slab.GpuBackend(ctx, p, self.FIELDS)
+        dev = self.backend.device
+        ex = slab.Exchanger(self.dist.pg, rank, world, periodic, dev)
+        self.rank_drv = slab.SlabRank(self.backend, ex, self.bounds, ncx, periodic)
+        self.n_active = int((rows[:, -1] == 0).sum())
+        N = float(len(rows))
+        self.kernels = {
+            200: ("density+EOS", (8.0 * d + 8 + 8) * N, 0.0),
+            201: ("momentum G11+A", (8.0 * d * 3 + 16) * N, 0.0),
+            301: ("symplectic integrator", (8.0 * (4 * d + 1) + 8 * 2 * d) * N, 20.0 * N),
+            300: ("cell build", (8.0 * d + 8 + 60 + 4 + 16 * (3 * d + 5)) * N, 0.0),
+        }
+        self.cand_per_particle = float("nan")
+        self.nbr_per_particle = float("nan")
+        self.h_rows = torch.from_numpy(rows).pin_memory()
+        self.h_out = torch.empty_like(self.h_rows).pin_memory()
+        self.h2d = self.h_rows.numel() * 8
+        self.d2h = self.h_rows.numel() * 8
+
+    def step(self, ctx):
+        self.rank_drv.step()
+
+    def e2e_step(self, ctx):
+        import torch
+        dev_rows = self.h_rows.to(self.backend.device, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        self.backend.load(dev_rows)
+        self.step(ctx)
+        local = self.backend.select(-(1 << 30), 1 << 30, 0)
+        m = min(local.shape[0], self.h_out.shape[0])
+        self.h_out[:m].copy_(local[:m], non_blocking=False)
+
+    def config(self):
+        c = super().config()
+        c.pop("candidates_per_particle", None)
+        c.pop("neighbours_per_particle", None)
+        c["slabs"] = self.bounds
+        c["ghost_planes"] = 2
+        return c
+
+
+def make_workload(cfg, dist=None, slab=False):
+    if slab and cfg in (0, 2):
+        return DamBreakSlab(3 if cfg == 2 else 2, dist)
     return {1: Microbench, 2: lambda: DamBreak(3), 0: lambda: DamBreak(2)}[cfg]()
 
 
@@ -374,7 +461,8 @@ def run_ours(args, dist):
     import torch
     from paper_1710_08259_b200 import nau
 
-    wl = make_workload(args.config)
+    use_slab = args.config in (0, 2) and (args.slab or dist.world > 1)
+    wl = make_workload(args.config, dist, use_slab)
     ctx = nau.Context(dist.local)
     ctx.set_mode(args.mode == "fast")
     wl.setup(ctx)
@@ -441,9 +529,12 @@ def run_ours(args, dist):
         "metric": METRIC, "value": round(value, 1), "unit": "particle-updates/s",
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if use_slab else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": dict(wl.config(), mode=args.mode,
-                       parallelism="replicas" if dist.world > 1 else "single GPU",
+                       parallelism=(f"x-slabs over {dist.world} GPU(s), NCCL halo+migration"
+                                    if use_slab else
+                                    ("replicas" if dist.world > 1 else "single GPU")),
                        l2="flushed between timed steps (256 MiB memset, untimed)"),
         "e2e": {"value": round(e2e, 1), "unit": "particle-updates/s",
                 "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h),
@@ -455,6 +546,13 @@ def run_ours(args, dist):
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, wl)
+    # torch tensors allocated inside the ExternalStream(ctx stream) regions must be
+    # released before the context destroys that stream
+    import gc
+    torch.cuda.synchronize()
+    wl = None
+    gc.collect()
+    torch.cuda.synchronize()
     ctx.close()
     return line
 

@@ -188,6 +188,22 @@ nau_status nau_wcsph_step(nau_ctx* ctx, const nau_wcsph_params* prm);
  * kind: 0 max, 1 min, 2 sum, 3 mean; out has rows*cols doubles (max/min: 1). */
 nau_status nau_reduce(nau_ctx* ctx, int kind, int field_id, double* out);
 
+/* ---- multi-GPU slab decomposition (no reference counterpart:
+ * the reference has no domain decomposition) ----
+ * Rows are particle-major: every live field in id order (r first), rows x cols
+ * doubles each; nau_row_width() doubles per particle. Device pointers. */
+int nau_row_width(nau_ctx* ctx);
+/* Slots (cell order) of active particles whose cell index along `axis`
+ * (particle_system.cpp:20-31) is in [lo, hi) and, if flag_field >= 0,
+ * flag_lo <= flag <= flag_hi; ascending slot order. Syncs. */
+nau_status nau_select(nau_ctx* ctx, int axis, double lo, double hi, int flag_field,
+                      double flag_lo, double flag_hi, int* dev_slots, long* count);
+nau_status nau_pack_rows(nau_ctx* ctx, const int* dev_slots, long m, double* dev_rows);
+/* Replace all particles by m rows (all active). gid_field >= 0 names a scalar
+ * field holding global particle indices: cells then list particles in ascending
+ * global index, so sums keep the single-GPU order. Marks cells dirty. */
+nau_status nau_load_rows(nau_ctx* ctx, const double* dev_rows, long m, int gid_field);
+
 /* Surfaces latched device errors (≙ the exceptions above). */
 nau_status nau_sync(nau_ctx* ctx);
 /* Message of the last error and the lowest original particle index involved (-1 if none). */

@@ -75,7 +75,64 @@ void free_particles(nau_ctx* c) {
     dfree(c->d_xl);
     dfree(c->d_aux);
     dfree(c->d_p4);
+    dfree(c->d_skey);
+    dfree(c->d_skey_s);
+    c->cap = 0;
 }
+
+nau_status ensure_field_storage(nau_ctx* c, FieldBuf& f);
+
+}  // namespace
+
+namespace nau {
+
+// Per-particle arrays (not fields) with capacity `cap` (>= n).
+nau_status alloc_particle_arrays(nau_ctx* c, long cap) {
+    c->cap = cap;
+    NAU_CUDA(dalloc(&c->d_orig, cap));
+    NAU_CUDA(dalloc(&c->d_orig_s, cap));
+    NAU_CUDA(dalloc(&c->d_key, cap));
+    NAU_CUDA(dalloc(&c->d_key_s, cap));
+    NAU_CUDA(dalloc(&c->d_active, cap));
+    NAU_CUDA(dalloc(&c->d_active_s, cap));
+    NAU_CUDA(dalloc(&c->d_perm, cap));
+    NAU_CUDA(dalloc(&c->d_perm_tmp, cap));
+    NAU_CUDA(dalloc(&c->d_okey, cap));
+    NAU_CUDA(dalloc(&c->d_xl, cap));
+    NAU_CUDA(dalloc(&c->d_aux, cap));
+    NAU_CUDA(dalloc(&c->d_p4, cap));
+    NAU_CUDA(dalloc(&c->d_skey, cap));
+    NAU_CUDA(dalloc(&c->d_skey_s, cap));
+    return NAU_OK;
+}
+
+// Grow every per-particle array and field to hold `m` particles (contents dropped).
+nau_status grow_capacity(nau_ctx* c, long m) {
+    if (m <= c->cap) return NAU_OK;
+    cudaStreamSynchronize(c->stream);
+    const long cap = std::max(m, c->cap + c->cap / 4);
+    std::vector<FieldBuf> fields = c->fields;  // shapes and liveness survive
+    c->fields.clear();
+    free_particles(c);  // per-particle arrays
+    for (auto& f : fields) {  // old field storage
+        dfree(f.d);
+        dfree(f.alt);
+    }
+    nau_status s = alloc_particle_arrays(c, cap);
+    if (s != NAU_OK) return s;
+    for (auto& f : fields) {
+        if (f.live) {
+            s = ensure_field_storage(c, f);
+            if (s != NAU_OK) return s;
+        }
+        c->fields.push_back(f);
+    }
+    return NAU_OK;
+}
+
+}  // namespace nau
+
+namespace {
 
 void free_cells(nau_ctx* c) {
     dfree(c->d_cell_start);
@@ -150,7 +207,7 @@ nau_status collect(nau_ctx* c) {
 }
 
 nau_status ensure_field_storage(nau_ctx* c, FieldBuf& f) {
-    long len = (long)f.comps() * c->n;
+    long len = (long)f.comps() * c->cap;
     NAU_CUDA(dalloc(&f.d, len));
     NAU_CUDA(dalloc(&f.alt, len));
     NAU_CUDA(cudaMemsetAsync(f.d, 0, sizeof(double) * (len ? len : 1), c->stream));
@@ -353,21 +410,12 @@ nau_status nau_set_particles(nau_ctx* c, long n, const double* pos_soa) {
     cudaStreamSynchronize(c->stream);
     free_particles(c);
     c->n = n;
-    NAU_CUDA(dalloc(&c->d_orig, n));
-    NAU_CUDA(dalloc(&c->d_orig_s, n));
-    NAU_CUDA(dalloc(&c->d_key, n));
-    NAU_CUDA(dalloc(&c->d_key_s, n));
-    NAU_CUDA(dalloc(&c->d_active, n));
-    NAU_CUDA(dalloc(&c->d_active_s, n));
-    NAU_CUDA(dalloc(&c->d_perm, n));
-    NAU_CUDA(dalloc(&c->d_perm_tmp, n));
-    NAU_CUDA(dalloc(&c->d_okey, n));
-    NAU_CUDA(dalloc(&c->d_xl, n));
-    NAU_CUDA(dalloc(&c->d_aux, n));
-    NAU_CUDA(dalloc(&c->d_p4, n));
+    nau_status sa = nau::alloc_particle_arrays(c, n);
+    if (sa != NAU_OK) return sa;
     if (n > 0) {
         k_iota<<<(int)((n + 255) / 256), 256, 0, c->stream>>>(n, c->d_orig);
-        c->launches++;
+        k_iota<<<(int)((n + 255) / 256), 256, 0, c->stream>>>(n, c->d_skey);
+        c->launches += 2;
     }
     NAU_CUDA(cudaMemsetAsync(c->d_active, 1, n ? n : 1, c->stream));
     FieldBuf r;

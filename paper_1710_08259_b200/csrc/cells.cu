@@ -177,12 +177,14 @@ struct ReorderTable {
 // conservative pre-filter input of sweep.cuh / sweep_fast.cuh (NaN when inactive).
 __global__ void k_reorder(DomainDev d, long n, const int* perm, const int* orig, const int* key,
                           const uint8_t* active, int* orig_s, int* key_s, uint8_t* active_s,
-                          float4* xl, double4* p4, ReorderTable t) {
+                          float4* xl, double4* p4, const int* skey, int* skey_s,
+                          ReorderTable t) {
     long s = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (s >= n) return;
     int k = perm[s];
     const int kk = key[k];
     orig_s[s] = orig[k];
+    skey_s[s] = skey[k];
     key_s[s] = kk;
     active_s[s] = active[k];
     for (int f = 0; f < t.nf; ++f) {
@@ -263,8 +265,9 @@ void launch_build_cells(nau_ctx* c) {
     // cell_start[ncells] (start of the inactive tail bin) = number of active particles.
     scan_exclusive(c, c->d_cell_count, c->d_cell_start, nc + 1);
     if (n == 0) return;
-    k_scatter<<<blocks_for(n), kBlock, 0, c->stream>>>(n, c->d_key, c->d_orig, c->d_cell_start,
+    k_scatter<<<blocks_for(n), kBlock, 0, c->stream>>>(n, c->d_key, c->d_skey, c->d_cell_start,
                                                        c->d_cursor, c->d_perm_tmp, c->d_okey);
+    // (okey = the within-cell sort key: original index, or a slab's global id)
     k_rank<<<blocks_for(n), kBlock, 0, c->stream>>>(n, nc, c->d_key, c->d_cell_start,
                                                     c->d_cell_count, c->d_perm_tmp, c->d_okey,
                                                     c->d_perm);
@@ -279,9 +282,11 @@ void launch_build_cells(nau_ctx* c) {
     }
     k_reorder<<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->d_perm, c->d_orig, c->d_key,
                                                        c->d_active, c->d_orig_s, c->d_key_s,
-                                                       c->d_active_s, c->d_xl, c->d_p4, t);
+                                                       c->d_active_s, c->d_xl, c->d_p4,
+                                                       c->d_skey, c->d_skey_s, t);
     c->launches += 3;
     std::swap(c->d_orig, c->d_orig_s);
+    std::swap(c->d_skey, c->d_skey_s);
     std::swap(c->d_key, c->d_key_s);
     std::swap(c->d_active, c->d_active_s);
     for (auto& fb : c->fields)

@@ -313,6 +313,7 @@ struct nau_ctx {
     bool has_domain = false;
     nau::DomainDev dom{};
     long n = 0;
+    long cap = 0;  // allocated particle capacity (>= n); SoA strides use n
     std::vector<nau::FieldBuf> fields;
     int* d_orig = nullptr;
     int* d_orig_s = nullptr;
@@ -323,6 +324,8 @@ struct nau_ctx {
     int* d_perm = nullptr;
     int* d_perm_tmp = nullptr;
     int* d_okey = nullptr;
+    int* d_skey = nullptr;    // within-cell sort key (original index, or a global id in slabs)
+    int* d_skey_s = nullptr;
     float4* d_xl = nullptr;  // fp32 global-origin coordinates (sweep pre-filters)
     double4* d_aux = nullptr;  // per-particle scratch (fast WCSPH: v and p / rho^2 packed)
     double4* d_p4 = nullptr;  // packed positions (written by the reorder pass)
@@ -350,6 +353,8 @@ struct nau_ctx {
 
 // Launch helpers shared by the .cu files (implemented in capi.cu).
 namespace nau {
+nau_status alloc_particle_arrays(nau_ctx* c, long cap);
+nau_status grow_capacity(nau_ctx* c, long m);
 Geo make_geo(nau_ctx* c);
 Opd make_opd(nau_ctx* c, const nau_operand& o);
 void prof_begin(nau_ctx* c, int cls);

@@ -37,6 +37,7 @@ EXPORTS = [
     "nau_cell_tables", "nau_neighbor_counts", "nau_interact", "nau_euler", "nau_symplectic_step",
     "nau_wcsph_step", "nau_reduce", "nau_sync", "nau_last_error", "nau_profile_enable",
     "nau_profile_ms", "nau_launch_count", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
+    "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows",
 ]
 
 
@@ -119,6 +120,10 @@ def load():
         "nau_fp64_peak_tflops": (d, [i]),
         "nau_set_mode": (i, [vp, i]),
         "nau_get_mode": (i, [vp]),
+        "nau_row_width": (i, [vp]),
+        "nau_select": (i, [vp, i, d, d, i, d, d, vp, C.POINTER(l)]),
+        "nau_pack_rows": (i, [vp, vp, l, vp]),
+        "nau_load_rows": (i, [vp, vp, l, i]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -336,3 +336,68 @@ def test_fast_mode_dam_break_vs_port(ctx):
                 assert rel_err(ctx.download(k), st[k]) <= tol, (s, k)
     ctx.set_mode(False)
     np.testing.assert_array_equal(ctx.active(), ps.active)
+
+
+# ------------------------------------------------------- slab primitives ----
+def test_select_pack_load_roundtrip(ctx):
+    import torch
+    rng = np.random.default_rng(21)
+    spec = cases.random_spec(rng, dim=3, n=5000, kinds=[0, 1, 2], cells=[5, 4, 3])
+    spec["fields"]["gid"] = (np.arange(5000)[::-1].astype(np.float64) * 3).reshape(1, -1)
+    cases.gpu_context(spec, ctx)
+    W = ctx.L.nau_row_width(ctx.h)
+    assert W == 3 + 1 + 3 + 1 + 1 + 1 + 1
+    slots = torch.empty(5000, dtype=torch.int32, device="cuda")
+    import ctypes as C
+    cnt = C.c_long(0)
+    assert ctx.L.nau_select(ctx.h, 0, 1.0, 3.0, -1, 0.0, 0.0, slots.data_ptr(), C.byref(cnt)) == 0
+    cx = np.floor(spec["pos"][0] / 0.3).astype(int) % 5
+    assert cnt.value == int(((cx >= 1) & (cx < 3)).sum())
+    rows = torch.empty((cnt.value, W), dtype=torch.float64, device="cuda")
+    assert ctx.L.nau_pack_rows(ctx.h, slots.data_ptr(), cnt.value, rows.data_ptr()) == 0
+    h = rows.cpu().numpy()
+    sel = np.nonzero((cx >= 1) & (cx < 3))[0]
+    # columns: r(3) A V(3) rho M Rp gid -> gid is the last column here
+    exp = np.concatenate([spec["pos"], spec["fields"]["A"], spec["fields"]["V"],
+                          spec["fields"]["rho"], spec["fields"]["M"], spec["fields"]["Rp"],
+                          spec["fields"]["gid"]], axis=0).T[sel]
+    np.testing.assert_array_equal(h[np.argsort(h[:, -1])], exp[np.argsort(exp[:, -1])])
+    # reload only those rows keyed by gid: cells list them in ascending gid
+    assert ctx.L.nau_load_rows(ctx.h, rows.data_ptr(), cnt.value, ctx.fields["gid"].id) == 0
+    ctx.n = cnt.value
+    _, start, count, srt = ctx.cell_tables()
+    gid_of_local = ctx.download("gid")[0]
+    for c in np.nonzero(count)[0][:50]:
+        g = gid_of_local[srt[start[c]:start[c] + count[c]]]
+        assert np.all(np.diff(g) > 0)
+
+
+def test_slab_path_single_rank_matches_plain(ctx):
+    """The slab driver (select/pack/load every step) on one GPU = the plain path, bitwise."""
+    import bench
+    from paper_1710_08259_b200 import slab as slab_mod
+
+    class D:
+        world, rank, local, pg = 1, 0, 0, None
+
+    plain = bench.DamBreak(2)
+    plain.sc = scenes.dam_break(2, dx=0.05, fluid=(1.0, 1.0), tank=(2.0, 1.6))
+    plain.sc.fields["v"][0, : plain.sc.params["n_fluid"]] = 3.0
+    ctx.set_mode(False)
+    plain.setup(ctx)
+    for _ in range(8):
+        plain.step(ctx)
+    ref_r, ref_v = ctx.download("r"), ctx.download("v")
+    ctx2 = nau.Context(0)
+    sl = bench.DamBreakSlab(2, D())
+    sl.sc = plain.sc = scenes.dam_break(2, dx=0.05, fluid=(1.0, 1.0), tank=(2.0, 1.6))
+    sl.sc.fields["v"][0, : sl.sc.params["n_fluid"]] = 3.0
+    sl.setup(ctx2)
+    for _ in range(8):
+        sl.step(ctx2)
+    gid = ctx2.download("gid")[0].astype(int)
+    r2, v2 = np.empty_like(ref_r), np.empty_like(ref_v)
+    r2[:, gid], v2[:, gid] = ctx2.download("r"), ctx2.download("v")
+    np.testing.assert_array_equal(r2, ref_r)
+    np.testing.assert_array_equal(v2, ref_v)
+    ctx2.close()
