@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=[0, 1, 2])
+    ap.add_argument("--config", type=int, default=2, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the bounded reference sample")
@@ -348,6 +348,110 @@ class DamBreak(Workload):
                 "neighbours_per_particle": round(self.nbr_per_particle, 2)}
 
 
+class DemColumn(Workload):
+    """BASELINE cfg3: 2 M spheres settling (linear spring-dashpot + Coulomb, mirror walls)."""
+
+    def __init__(self):
+        from paper_1710_08259_b200 import scenes
+        self.sc = scenes.dem_column()
+        self.name = ("cfg3: 3D DEM granular settling, 2,000,000 spheres, log-normal radii, "
+                     "linear spring-dashpot + Coulomb, dt=1e-6")
+
+    def setup(self, ctx):
+        from paper_1710_08259_b200 import nau
+        sc, prm = self.sc, self.sc.params
+        ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+        ctx.set_particles(sc.pos)
+        for k in ("v", "vdot", "R", "m"):
+            v = np.asarray(sc.fields[k]).reshape(-1, sc.n)
+            ctx.add_field(k, v.shape[0], 1, v)
+        ctx.boundary_shift()
+        ctx.build_cells()
+        p = nau.DemParams()
+        f = ctx.fields
+        p.law, p.f_v, p.f_vdot, p.f_R, p.f_m = 8, f["v"].id, f["vdot"].id, f["R"].id, f["m"].id
+        p.P, p.Q, p.cf, p.search_radius, p.dt = prm["kn"], prm["en"], prm["cf"], \
+            prm["search_radius"], prm["dt"]
+        for a in range(3):
+            p.g[a] = prm["g"][a]
+        self.p = p
+        C = stencil_candidates(ctx, 3)
+        N = float(sc.n)
+        self.n_active = sc.n
+        self.kernels = {
+            108: ("dem_lsd contact sum", 88.0 * N, 8 * C),
+            301: ("symplectic integrator", 8.0 * 22 * N, 20.0 * N),
+            300: ("cell build", (24.0 + 8 + 60 + 4 + 16 * 11) * N, 0.0),
+        }
+        self.cand_per_particle = C / N
+        import torch
+        self.h_r = torch.from_numpy(np.ascontiguousarray(sc.pos)).pin_memory()
+        self.h_v = torch.zeros((3, sc.n), dtype=torch.float64).pin_memory()
+        self.h_out = {k: torch.empty((3, sc.n), dtype=torch.float64).pin_memory() for k in ("r", "v")}
+        self.h2d = (self.h_r.numel() + self.h_v.numel()) * 8
+        self.d2h = sum(t.numel() for t in self.h_out.values()) * 8
+
+    def step(self, ctx):
+        ctx.dem_step(self.p)
+
+    def e2e_step(self, ctx):
+        ctx.upload_ptr("r", self.h_r.data_ptr())
+        ctx.upload_ptr("v", self.h_v.data_ptr())
+        self.step(ctx)
+        for k, t in self.h_out.items():
+            ctx.download_ptr(k, t.data_ptr())
+
+    def config(self):
+        sc = self.sc
+        return {"workload": self.name, "particles": sc.n, "cells": "x".join(map(str, sc.max_cells)),
+                "dt": sc.params["dt"], "candidates_per_particle": round(self.cand_per_particle, 2)}
+
+
+class Gravity(Workload):
+    """BASELINE cfg4: Plummer sphere, direct all-pairs softened gravity, leapfrog."""
+
+    def __init__(self):
+        from paper_1710_08259_b200 import scenes
+        self.sc = scenes.plummer()
+        self.name = "cfg4: 3D n-body Plummer sphere, N=262,144, eps=0.01, leapfrog dt=1e-3"
+
+    def setup(self, ctx):
+        from paper_1710_08259_b200 import nau
+        sc, prm = self.sc, self.sc.params
+        ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+        ctx.set_particles(sc.pos)
+        ctx.add_field("v", 3, 1, sc.fields["v"])
+        ctx.add_field("a", 3, 1, 0.0)
+        ctx.boundary_shift()
+        p = nau.GravityParams()
+        p.f_v, p.f_a, p.f_m = ctx.fields["v"].id, ctx.fields["a"].id, -1
+        p.m, p.G, p.eps, p.dt = prm["m"], prm["G"], prm["eps"], prm["dt"]
+        self.p = p
+        ctx.interact("nbody_gravity", [prm["m"], prm["G"], prm["eps"]], "a")  # a(t=0)
+        N = float(sc.n)
+        self.n_active = sc.n
+        self.kernels = {107: ("all-pairs gravity", 56.0 * N, 20.0 * N * N)}
+        import torch
+        self.h_r = torch.from_numpy(np.ascontiguousarray(sc.pos)).pin_memory()
+        self.h_v = torch.from_numpy(np.ascontiguousarray(sc.fields["v"])).pin_memory()
+        self.h_out = {k: torch.empty((3, sc.n), dtype=torch.float64).pin_memory() for k in ("r", "v")}
+        self.h2d = (self.h_r.numel() + self.h_v.numel()) * 8
+        self.d2h = sum(t.numel() for t in self.h_out.values()) * 8
+
+    def step(self, ctx):
+        ctx.leapfrog_step(self.p)
+
+    def e2e_step(self, ctx):
+        ctx.upload_ptr("r", self.h_r.data_ptr())
+        ctx.upload_ptr("v", self.h_v.data_ptr())
+        self.step(ctx)
+        for k, t in self.h_out.items():
+            ctx.download_ptr(k, t.data_ptr())
+
+    def config(self):
+        return {"workload": self.name, "particles": self.sc.n, "pairs_per_step": self.sc.n ** 2}
+
+
 class DamBreakSlab(DamBreak):
     """cfg2/cfg0 slab-decomposed along x over the ranks (paper_1710_08259_b200/slab.py):
     each rank owns whole x-cell planes (balanced on particle counts) plus two ghost
@@ -434,7 +538,8 @@ class DamBreakSlab(DamBreak):
 def make_workload(cfg, dist=None, slab=False):
     if slab and cfg in (0, 2):
         return DamBreakSlab(3 if cfg == 2 else 2, dist)
-    return {1: Microbench, 2: lambda: DamBreak(3), 0: lambda: DamBreak(2)}[cfg]()
+    return {1: Microbench, 2: lambda: DamBreak(3), 0: lambda: DamBreak(2), 3: DemColumn,
+            4: Gravity}[cfg]()
 
 
 # ------------------------------------------------------------ timing ----
@@ -575,6 +680,31 @@ def cpu_baseline(args, wl=None):
                  "sph_L0(A,m,rho,Wp53220,R)"]
         comps = [1, 3, 1]
         kernel_note = "Wendland Wp53220 (the reference has no cubic spline; same candidate loop)"
+    elif args.config == 3:
+        from paper_1710_08259_b200 import scenes
+        sc = wl.sc if wl else scenes.dem_column()
+        prm = sc.params
+        rc = ref.RefCase(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds, sc.pos)
+        rng = np.random.default_rng(0)
+        rc.field("v", rng.uniform(-0.01, 0.01, (3, sc.n))).field("vdot", sc.fields["vdot"])
+        rc.field("R", sc.fields["R"]).field("m", sc.fields["m"])
+        rc.constant("E", 2.06e6).constant("nu", 0.33).constant("cf", prm["cf"])
+        rc.constant("Rs", prm["search_radius"]).constant("g", prm["g"]).variable("dt", prm["dt"])
+        exprs = ["dem_l(v,R,E,nu,m,cf,Rs)+g", "euler(v,vdot,dt)", "euler(r,v,dt)"]
+        comps = [3, 3, 3]
+        kernel_note = ("the reference's stock Hertz dem_l through the same contact loop "
+                       "(it has no linear spring-dashpot law)")
+    elif args.config == 4:
+        from paper_1710_08259_b200 import scenes
+        sc = wl.sc if wl else scenes.plummer()
+        prm = sc.params
+        rc = ref.RefCase(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds, sc.pos)
+        rc.field("v", sc.fields["v"]).field("a", sc.fields["a"])
+        rc.constant("m", prm["m"]).constant("G", prm["G"]).constant("eps", prm["eps"])
+        rc.variable("dth", 0.5 * prm["dt"]).variable("dt", prm["dt"])
+        exprs = ["euler(v,a,dth)", "euler(r,v,dt)", "nbody_gravity(m,G,eps)", "euler(v,a,dth)"]
+        comps = [3, 3, 3, 3]
+        kernel_note = "nbody_gravity all pairs (interactions.cpp:195-214), leapfrog as equation order"
     else:
         from paper_1710_08259_b200 import scenes
         sc = wl.sc if wl else (scenes.dam_break(3, dx=0.005) if args.config == 2
@@ -638,13 +768,13 @@ def cpu_baseline_port(args):
 def run_reference(args, dist):
     if dist.rank != 0:
         return None
-    wl_name = {1: "cfg1", 2: "cfg2", 0: "cfg0"}[args.config]
+    wl_name = {1: "cfg1", 2: "cfg2", 0: "cfg0", 3: "cfg3", 4: "cfg4"}[args.config]
     cb = cpu_baseline(args)
     per_step_ms = None
     if cb["value"]:
         from paper_1710_08259_b200 import scenes
-        n = (scenes.sph_microbench().n if args.config == 1 else
-             (scenes.dam_break(3, dx=0.005).n if args.config == 2 else scenes.dam_break(2).n))
+        n = {1: lambda: scenes.sph_microbench().n, 2: lambda: scenes.dam_break(3, dx=0.005).n,
+             0: lambda: scenes.dam_break(2).n, 3: lambda: 2_000_000, 4: lambda: 262_144}[args.config]()
         per_step_ms = n / cb["value"] * 1e3
     return {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "particle-updates/s",
             "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms,

@@ -184,6 +184,28 @@ typedef struct {
 } nau_wcsph_params;
 nau_status nau_wcsph_step(nau_ctx* ctx, const nau_wcsph_params* prm);
 
+/* DEM deck (BASELINE cfg3), the reference's equation form:
+ *   vdot = law(v, R, P, Q, m, cf, Rs) + g;  v = euler(v, vdot, dt);  r = euler(r, v, dt)
+ * law = NAU_OP_DEM_LSD (P = kn, Q = en) or NAU_OP_DEM_HERTZ (P = E, Q = nu);
+ * f_R / f_m = -1 use the uniform R / m. Boundary shift after the r update. */
+typedef struct {
+    int law;
+    int f_v, f_vdot, f_R, f_m;
+    double R, m, P, Q, cf, search_radius, dt;
+    double g[3];
+} nau_dem_params;
+nau_status nau_dem_step(nau_ctx* ctx, const nau_dem_params* prm);
+
+/* Leapfrog all-pairs gravity (BASELINE cfg4), kick-drift-kick as equation order:
+ *   v = euler(v, a, dt/2); r = euler(r, v, dt); a = nbody_gravity(m, G, eps);
+ *   v = euler(v, a, dt/2).   f_m = -1 uses the uniform m. No cells are built
+ * (nbody_gravity has finite_influence = false, interactions.cpp:267). */
+typedef struct {
+    int f_v, f_a, f_m;
+    double m, G, eps, dt;
+} nau_gravity_params;
+nau_status nau_leapfrog_step(nau_ctx* ctx, const nau_gravity_params* prm);
+
 /* ≙ ReductionNode fsum/fmax/fmin/fmean over active particles (sfl/ast.cpp:237-274).
  * kind: 0 max, 1 min, 2 sum, 3 mean; out has rows*cols doubles (max/min: 1). */
 nau_status nau_reduce(nau_ctx* ctx, int kind, int field_id, double* out);

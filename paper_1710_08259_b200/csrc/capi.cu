@@ -724,6 +724,57 @@ nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
     return NAU_OK;
 }
 
+static void set_operand(nau_operand& o, int field_id, double uniform) {
+    std::memset(&o, 0, sizeof(o));
+    o.field_id = field_id;
+    o.rows = 1;
+    o.cols = 1;
+    o.value[0] = uniform;
+}
+
+nau_status nau_dem_step(nau_ctx* c, const nau_dem_params* p) {
+    if (p->law != NAU_OP_DEM_LSD && p->law != NAU_OP_DEM_HERTZ)
+        return fail(c, NAU_ERR_ARG, "nau_dem_step: law must be dem_lsd or dem_l");
+    if (!field_ok(c, p->f_v) || !field_ok(c, p->f_vdot) || (p->f_R >= 0 && !field_ok(c, p->f_R)) ||
+        (p->f_m >= 0 && !field_ok(c, p->f_m)))
+        return fail(c, NAU_ERR_ARG, "bad field id");
+    if (c->dirty || !c->built_once) {
+        nau_status s = nau_build_cells(c);
+        if (s != NAU_OK) return s;
+    }
+    nau_operand ops[7];
+    set_operand(ops[0], p->f_v, 0.0);
+    set_operand(ops[1], p->f_R, p->R);
+    set_operand(ops[2], -1, p->P);
+    set_operand(ops[3], -1, p->Q);
+    set_operand(ops[4], p->f_m, p->m);
+    set_operand(ops[5], -1, p->cf);
+    set_operand(ops[6], -1, p->search_radius);
+    nau::Opd d_ops[7];
+    for (int k = 0; k < 7; ++k) d_ops[k] = nau::make_opd(c, ops[k]);
+    const int dim = c->dom.dim;
+    nau::launch_interact(c, p->law, 0, 0, d_ops, 7, c->fields[p->f_vdot].d, dim, 1, dim, 1, p->g);
+    nau::launch_symplectic(c, c->fields[p->f_v].d, c->fields[p->f_vdot].d, nullptr, p->dt);
+    c->dirty = true;
+    return NAU_OK;
+}
+
+nau_status nau_leapfrog_step(nau_ctx* c, const nau_gravity_params* p) {
+    if (!field_ok(c, p->f_v) || !field_ok(c, p->f_a) || (p->f_m >= 0 && !field_ok(c, p->f_m)))
+        return fail(c, NAU_ERR_ARG, "bad field id");
+    const double dth = 0.5 * p->dt;
+    nau_status s = nau_euler(c, p->f_v, p->f_a, dth, p->f_v);  // v = euler(v, a, dt/2)
+    if (s == NAU_OK) s = nau_euler(c, 0, p->f_v, p->dt, 0);     // r = euler(r, v, dt) + shift
+    if (s != NAU_OK) return s;
+    nau_operand ops[3];
+    set_operand(ops[0], p->f_m, p->m);
+    set_operand(ops[1], -1, p->G);
+    set_operand(ops[2], -1, p->eps);
+    s = nau_interact(c, NAU_OP_GRAVITY, 0, 0, ops, 3, p->f_a);  // a = nbody_gravity(m, G, eps)
+    if (s == NAU_OK) s = nau_euler(c, p->f_v, p->f_a, dth, p->f_v);  // v = euler(v, a, dt/2)
+    return s;
+}
+
 nau_status nau_set_mode(nau_ctx* c, int mode) {
     if (mode != NAU_MODE_EXACT && mode != NAU_MODE_FAST) return fail(c, NAU_ERR_ARG, "unknown mode");
     c->mode = mode;

@@ -174,6 +174,8 @@ struct DemArgs {
     const float4* xl;
     Opd v, R, P, Q, m, cf, Rs;  // P = E (Hertz) | kn (LSD); Q = nu (Hertz) | en (LSD)
     double zeta_uniform;        // LSD damping ratio from a uniform en (host libm), else NaN
+    double gadd[3];             // body acceleration added to the result (DEM deck: + g)
+    int has_g;
     double* out;
     DevErr* err;
 };
@@ -275,6 +277,7 @@ __global__ void __launch_bounds__(kThreads) k_dem(const __grid_constant__ DemArg
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
         double r = kImagesOnly ? acc[d] : acc[d] / mi;
+        if (a.has_g) r = r + a.gadd[d];  // vdot = dem_...(...) + g (BinaryNode Add)
         if (!isfinite(r)) latch_error(a.err, 2, kMsgNan, my_orig);
         a.out[d * n + k] = r;
     }
@@ -297,7 +300,8 @@ struct GravArgs {
     DevErr* err;
 };
 
-template <int DIM>
+// FAST: s = G m_j rsqrt(r2)^3 with FMA (≈1e-15 relative per pair); exact: G m_j / (r2 sqrt r2).
+template <int DIM, bool FAST>
 __global__ void __launch_bounds__(kGravTile) k_gravity(const __grid_constant__ GravArgs a) {
     __shared__ double sx[3][kGravTile];
     __shared__ double sm[kGravTile];
@@ -342,7 +346,13 @@ __global__ void __launch_bounds__(kGravTile) k_gravity(const __grid_constant__ G
                     coincident = true;
                     continue;
                 }
-                const double s = G * sm[t] / (r2 * sqrt(r2));
+                double s;
+                if (FAST) {
+                    const double inv = rsqrt(r2);
+                    s = G * sm[t] * (inv * inv * inv);
+                } else {
+                    s = G * sm[t] / (r2 * sqrt(r2));
+                }
 #pragma unroll
                 for (int d = 0; d < DIM; ++d) acc[d] = acc[d] + rel[d] * s;
             }
@@ -400,7 +410,7 @@ void dem_dispatch(nau_ctx* c, int op, const DemArgs& a) {
 }  // namespace
 
 void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int nops, double* out,
-                     int out_rows, int out_cols, int a_rows, int a_cols) {
+                     int out_rows, int out_cols, int a_rows, int a_cols, const double* gadd) {
     (void)out_rows;
     (void)out_cols;
     if (c->n == 0) return;
@@ -439,9 +449,17 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
         a.err = c->d_err;
         const int blocks = (int)((c->n + kGravTile - 1) / kGravTile);
         prof_begin(c, 100 + op);
-        if (dim == 1) k_gravity<1><<<blocks, kGravTile, 0, c->stream>>>(a);
-        else if (dim == 2) k_gravity<2><<<blocks, kGravTile, 0, c->stream>>>(a);
-        else k_gravity<3><<<blocks, kGravTile, 0, c->stream>>>(a);
+        const bool fast = c->mode == NAU_MODE_FAST;
+        if (dim == 1) {
+            if (fast) k_gravity<1, true><<<blocks, kGravTile, 0, c->stream>>>(a);
+            else k_gravity<1, false><<<blocks, kGravTile, 0, c->stream>>>(a);
+        } else if (dim == 2) {
+            if (fast) k_gravity<2, true><<<blocks, kGravTile, 0, c->stream>>>(a);
+            else k_gravity<2, false><<<blocks, kGravTile, 0, c->stream>>>(a);
+        } else {
+            if (fast) k_gravity<3, true><<<blocks, kGravTile, 0, c->stream>>>(a);
+            else k_gravity<3, false><<<blocks, kGravTile, 0, c->stream>>>(a);
+        }
         prof_end(c, 100 + op);
     } else {
         DemArgs a;
@@ -455,6 +473,8 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
         a.cf = ops[5];
         a.Rs = ops[6];
         a.zeta_uniform = __builtin_nan("");
+        a.has_g = gadd != nullptr;
+        for (int d = 0; d < 3; ++d) a.gadd[d] = gadd ? gadd[d] : 0.0;
         if (op == NAU_OP_DEM_LSD && ops[3].p == nullptr) {
             double le = std::log(ops[3].v[0]);
             a.zeta_uniform = -le / std::sqrt(kPi * kPi + le * le);

@@ -368,7 +368,8 @@ void launch_unsort(nau_ctx* c, const double* d_src, double* d_dst, int comps);
 void launch_sort_in(nau_ctx* c, const double* d_src_orig, double* d_dst, int comps);
 // interact.cu
 void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int nops,
-                     double* out, int out_rows, int out_cols, int a_rows, int a_cols);
+                     double* out, int out_rows, int out_cols, int a_rows, int a_cols,
+                     const double* gadd = nullptr);
 // integrate.cu
 void launch_euler(nau_ctx* c, const double* x, const double* xdot, double dt, double* out,
                   int comps);

@@ -37,7 +37,8 @@ EXPORTS = [
     "nau_cell_tables", "nau_neighbor_counts", "nau_interact", "nau_euler", "nau_symplectic_step",
     "nau_wcsph_step", "nau_reduce", "nau_sync", "nau_last_error", "nau_profile_enable",
     "nau_profile_ms", "nau_launch_count", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
-    "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows",
+    "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows", "nau_dem_step",
+    "nau_leapfrog_step",
 ]
 
 
@@ -66,6 +67,18 @@ class WcsphParams(C.Structure):
                 ("gamma", C.c_double), ("visc", C.c_double), ("dt", C.c_double),
                 ("g", C.c_double * 3), ("f_rho", C.c_int), ("f_p", C.c_int), ("f_v", C.c_int),
                 ("f_vdot", C.c_int), ("f_mask", C.c_int)]
+
+
+class DemParams(C.Structure):
+    _fields_ = [("law", C.c_int), ("f_v", C.c_int), ("f_vdot", C.c_int), ("f_R", C.c_int),
+                ("f_m", C.c_int), ("R", C.c_double), ("m", C.c_double), ("P", C.c_double),
+                ("Q", C.c_double), ("cf", C.c_double), ("search_radius", C.c_double),
+                ("dt", C.c_double), ("g", C.c_double * 3)]
+
+
+class GravityParams(C.Structure):
+    _fields_ = [("f_v", C.c_int), ("f_a", C.c_int), ("f_m", C.c_int), ("m", C.c_double),
+                ("G", C.c_double), ("eps", C.c_double), ("dt", C.c_double)]
 
 
 _lib = None
@@ -124,6 +137,8 @@ def load():
         "nau_select": (i, [vp, i, d, d, i, d, d, vp, C.POINTER(l)]),
         "nau_pack_rows": (i, [vp, vp, l, vp]),
         "nau_load_rows": (i, [vp, vp, l, i]),
+        "nau_dem_step": (i, [vp, C.POINTER(DemParams)]),
+        "nau_leapfrog_step": (i, [vp, C.POINTER(GravityParams)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -360,6 +375,12 @@ class Context:
 
     def wcsph_step(self, p: WcsphParams):
         self._check(self.L.nau_wcsph_step(self.h, C.byref(p)))
+
+    def dem_step(self, p: DemParams):
+        self._check(self.L.nau_dem_step(self.h, C.byref(p)))
+
+    def leapfrog_step(self, p: GravityParams):
+        self._check(self.L.nau_leapfrog_step(self.h, C.byref(p)))
 
     def reduce(self, kind, f):
         kinds = {"fmax": 0, "fmin": 1, "fsum": 2, "fmean": 3}

@@ -143,6 +143,84 @@ def dam_break(dim=2, dx=0.01, fluid=None, tank=None, layers=3, rho0=1000.0, grav
                 "n_fluid": n_f, "kernel_family": kernel_family})
 
 
+# ---------------------------------------------------------------- cfg3 ----
+def dem_column(n=2_000_000, seed=3, box=(0.3, 0.3, 1.2), median=1e-3, sigma=0.2,
+               rho_s=2500.0, kn=1e5, en=0.5, mu=0.5, dt=1e-6, gravity=9.81) -> Scene:
+    """BASELINE cfg3: n spheres, log-normal radii (median, sigma_log) from Box-Muller on
+    draws 0,1 of the reference RNG, settling under gravity in a column with
+    symmetric (mirror-image) walls — the floor is the z-low wall
+    (interactions.cpp:168-170 mirror mechanism). Linear spring-dashpot normal force
+    k_n, restitution e_n, Coulomb friction mu; cell = search radius = 2 r_max.
+
+    Stand-in for random sequential addition: a jittered cubic lattice with the
+    same number density; radii are clamped at 0.95 s/2 (s = lattice spacing,
+    about +3 sigma; 0.1% of the draws) so the jittered lattice never overlaps.
+    """
+    d = uniform_draws(seed, n, 5)
+    u1 = np.maximum(d[0], 2.0 ** -53)
+    z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * math.pi * d[1])
+    s = (box[0] * box[1] * box[2] / n) ** (1.0 / 3.0)
+    nx, ny = int(box[0] / s), int(box[1] / s)
+    nz = int(math.ceil(n / (nx * ny)))
+    s = min(box[0] / nx, box[1] / ny, box[2] / nz)
+    R = np.minimum(median * np.exp(sigma * z), 0.95 * 0.5 * s)
+    k = np.arange(n)
+    site = np.stack([(k % nx + 0.5) * s, ((k // nx) % ny + 0.5) * s, (k // (nx * ny) + 0.5) * s])
+    room = 0.5 * s - R  # jitter keeps every sphere inside its lattice cube
+    pos = np.ascontiguousarray(site + (2.0 * d[2:5] - 1.0) * room * 0.999)
+    rmax = float(R.max())
+    cs = 2.0 * rmax
+    cells = [int(math.ceil(b / cs)) for b in box]
+    m = rho_s * 4.0 / 3.0 * math.pi * R ** 3
+    return Scene("dem_column", 3, [0, 0, 0], cells, [cs] * 3, [1, 1, 1], pos,
+                 fields={"v": np.zeros((3, n)), "vdot": np.zeros((3, n)), "R": R, "m": m},
+                 params={"kn": kn, "en": en, "cf": mu, "dt": dt, "g": [0.0, 0.0, -gravity],
+                         "search_radius": cs, "rho_s": rho_s, "lattice": s})
+
+
+def dem_equations():
+    """The DEM deck as SFL equation text (dem_lsd is registered beside dem_l)."""
+    return [("accel", "vdot=dem_lsd(v,R,kn,en,m,cf,Rs)+g"), ("velocity", "v=euler(v,vdot,dt)"),
+            ("position", "r=euler(r,v,dt)")]
+
+
+# ---------------------------------------------------------------- cfg4 ----
+def plummer(n=262_144, seed=4, eps=0.01, dt=1e-3, rmax=10.0) -> Scene:
+    """BASELINE cfg4: Plummer sphere, G = M = a = 1, m = 1/n, seeded draws of the
+    reference RNG: inverse-CDF radius (truncated at rmax), isotropic directions,
+    speed q v_esc with q rejection-sampled from q^2 (1 - q^2)^(7/2); centre of mass
+    and momentum removed. A cut-off box far outside rmax (escapers deactivate,
+    particle_system.cpp:77-84)."""
+    tries = 64
+    d = uniform_draws(seed, n, 5 + 2 * tries)
+    xmax = (rmax * rmax / (1.0 + rmax * rmax)) ** 1.5
+    X = np.maximum(d[0] * xmax, 1e-300)
+    r = 1.0 / np.sqrt(X ** (-2.0 / 3.0) - 1.0)
+    ct = 2.0 * d[1] - 1.0
+    st = np.sqrt(np.maximum(0.0, 1.0 - ct * ct))
+    ph = 2.0 * math.pi * d[2]
+    pos = np.stack([r * st * np.cos(ph), r * st * np.sin(ph), r * ct])
+    q = np.full(n, 0.5)
+    done = np.zeros(n, bool)
+    for t in range(tries):
+        qt, yt = d[5 + 2 * t], 0.1 * d[6 + 2 * t]
+        acc = ~done & (yt < qt * qt * (1.0 - qt * qt) ** 3.5)
+        q[acc] = qt[acc]
+        done |= acc
+    vesc = math.sqrt(2.0) * (1.0 + r * r) ** -0.25
+    ct2 = 2.0 * d[3] - 1.0
+    st2 = np.sqrt(np.maximum(0.0, 1.0 - ct2 * ct2))
+    ph2 = 2.0 * math.pi * d[4]
+    v = np.stack([st2 * np.cos(ph2), st2 * np.sin(ph2), ct2]) * (q * vesc)
+    pos -= pos.mean(axis=1, keepdims=True)
+    v -= v.mean(axis=1, keepdims=True)
+    box = rmax + 5.0
+    return Scene("plummer", 3, [-1, -1, -1], [1, 1, 1], [box] * 3, [2, 2, 2],
+                 np.ascontiguousarray(pos),
+                 fields={"v": np.ascontiguousarray(v), "a": np.zeros((3, n))},
+                 params={"m": 1.0 / n, "G": 1.0, "eps": eps, "dt": dt})
+
+
 def wcsph_equations(scene: Scene, kernel_keyword=None):
     """The dam-break deck as SFL equation text (for the reference oracle)."""
     kw = kernel_keyword or f"Wp5{scene.dim}220"

@@ -401,3 +401,90 @@ def test_slab_path_single_rank_matches_plain(ctx):
     np.testing.assert_array_equal(r2, ref_r)
     np.testing.assert_array_equal(v2, ref_v)
     ctx2.close()
+
+
+# ------------------------------------------------------------- DEM / n-body ----
+def _dem_port_step(ps, st, prm, R, m):
+    """vdot = dem_lsd(v,R,kn,en,m,cf,Rs) + g; v = euler(v,vdot,dt); r = euler(r,v,dt); shift."""
+    act = ps.active.astype(bool)
+    if ps.tables is None:
+        ps.build_cells()
+    acc = ps.interact(port.DEM_LSD, [st["v"], R, prm["kn"], prm["en"], m, prm["cf"],
+                                     prm["search_radius"]], (3, 1))
+    g = np.asarray(prm["g"]).reshape(3, 1)
+    st["vdot"][:, act] = acc[:, act] + g
+    st["v"][:, act] = st["v"][:, act] + prm["dt"] * st["vdot"][:, act]
+    ps.pos[:, act] = ps.pos[:, act] + prm["dt"] * st["v"][:, act]
+    ps.boundary_shift()
+    ps.tables = None
+
+
+@pytest.mark.parametrize("fast", [False, True])
+def test_dem_deck_vs_port(ctx, fast):
+    """cfg3 deck on a small compressed column (many contacts, floor via mirror images):
+    EXACT mode bitwise (no libm transcendental in the linear law); FAST within 1e-10."""
+    sc = scenes.dem_column(n=6000, box=(0.03, 0.03, 0.06), dt=1e-5)
+    prm = sc.params
+    sc.pos[2] *= 0.6  # squeeze the column vertically: overlapping contacts from step 1
+    sc.fields["v"][:] = np.random.default_rng(3).uniform(-0.05, 0.05, (3, sc.n))
+    ctx.set_mode(fast)
+    ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+    ctx.set_particles(sc.pos)
+    for k in ("v", "vdot", "R", "m"):
+        ctx.add_field(k, np.asarray(sc.fields[k]).reshape(-1, sc.n).shape[0], 1, sc.fields[k])
+    ctx.boundary_shift()
+    p = nau.DemParams()
+    f = ctx.fields
+    p.law, p.f_v, p.f_vdot, p.f_R, p.f_m = 8, f["v"].id, f["vdot"].id, f["R"].id, f["m"].id
+    p.P, p.Q, p.cf, p.search_radius, p.dt = prm["kn"], prm["en"], prm["cf"], prm["search_radius"], prm["dt"]
+    for a in range(3):
+        p.g[a] = prm["g"][a]
+    dom = port.Domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+    ps = port.ParticleSystem(dom, sc.pos)
+    ps.boundary_shift()
+    st = {"v": sc.fields["v"].copy(), "vdot": np.zeros((3, sc.n))}
+    for s in range(5):
+        ctx.dem_step(p)
+        _dem_port_step(ps, st, prm, sc.fields["R"], sc.fields["m"])
+    assert np.abs(st["vdot"][2] - prm["g"][2]).max() > 1.0, "no contact forces: test is vacuous"
+    for k, ref_v in (("r", ps.pos), ("v", st["v"]), ("vdot", st["vdot"])):
+        got = ctx.download(k)
+        if fast:
+            assert rel_err(got, ref_v) <= TOL_STEP, k
+        else:
+            np.testing.assert_array_equal(got, ref_v, err_msg=k)
+    ctx.set_mode(False)
+
+
+def test_gravity_leapfrog_vs_port(ctx):
+    """cfg4 deck on N = 1024 Plummer bodies: 3 leapfrog steps within 1e-10 (pow vs r^1.5);
+    total momentum stays ~0."""
+    sc = scenes.plummer(n=1024)
+    prm = sc.params
+    ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+    ctx.set_particles(sc.pos)
+    ctx.add_field("v", 3, 1, sc.fields["v"])
+    ctx.add_field("a", 3, 1, 0.0)
+    ctx.boundary_shift()
+    ctx.interact("nbody_gravity", [prm["m"], prm["G"], prm["eps"]], "a")
+    p = nau.GravityParams()
+    p.f_v, p.f_a, p.f_m = ctx.fields["v"].id, ctx.fields["a"].id, -1
+    p.m, p.G, p.eps, p.dt = prm["m"], prm["G"], prm["eps"], prm["dt"]
+    dom = port.Domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+    ps = port.ParticleSystem(dom, sc.pos)
+    ps.boundary_shift()
+    v = sc.fields["v"].copy()
+    grav = lambda: ps.interact(port.GRAVITY, [prm["m"], prm["G"], prm["eps"]], (3, 1))
+    a = grav()
+    for s in range(3):
+        ctx.leapfrog_step(p)
+        v = v + (0.5 * prm["dt"]) * a
+        ps.pos = ps.pos + prm["dt"] * v
+        ps.tables = None
+        a = grav()
+        v = v + (0.5 * prm["dt"]) * a
+    assert rel_err(ctx.download("r"), ps.pos) <= TOL_STEP
+    assert rel_err(ctx.download("v"), v) <= TOL_STEP
+    assert rel_err(ctx.download("a"), a) <= TOL_STEP
+    mom = ctx.download("v").sum(axis=1) * prm["m"]
+    assert np.abs(mom).max() <= 1e-12
