@@ -331,7 +331,26 @@ __global__ void __launch_bounds__(kGravTile) k_gravity(const __grid_constant__ G
             sa[threadIdx.x] = 0;
         }
         __syncthreads();
-        if (mine) {
+        if (mine && FAST) {
+            // branch-free pair loop (FMA via explicit fma(); this TU is -fmad=false):
+            // self / inactive pairs are masked, not skipped, so the loop unrolls.
+            const int lim = (int)min((long)kGravTile, n - base);
+#pragma unroll 4
+            for (int t = 0; t < lim; ++t) {
+                double rel[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+                for (int d = 0; d < DIM; ++d) rel[d] = sx[d][t] - xi[d];
+                double r2 = eps2;
+#pragma unroll
+                for (int d = DIM - 1; d >= 0; --d) r2 = fma(rel[d], rel[d], r2);
+                const bool ok = (base + t != k) && sa[t];
+                coincident |= ok && r2 == 0.0;
+                const double inv = rsqrt(ok && r2 > 0.0 ? r2 : 1.0);
+                const double s = ok && r2 > 0.0 ? G * sm[t] * (inv * inv * inv) : 0.0;
+#pragma unroll
+                for (int d = 0; d < DIM; ++d) acc[d] = fma(rel[d], s, acc[d]);
+            }
+        } else if (mine) {
             const int lim = (int)min((long)kGravTile, n - base);
             for (int t = 0; t < lim; ++t) {
                 if (base + t == k || !sa[t]) continue;

@@ -96,13 +96,13 @@ __device__ __forceinline__ void option_of(const DomainDev& d, int a, int ci, con
 // The sweep. Must be called by all 32 lanes of a warp (valid = false for lanes
 // without a particle). `pre_r` is the pre-filter radius (>= the operator's
 // acceptance radius).
-template <int DIM, bool ORDERED, class Fn>
-__device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ xl4, int k,
-                                      bool valid, const double* xi, float pre_r, Fn&& fn) {
-    __shared__ SweepSmem smem[kSweepThreads / 32];
+template <int DIM, bool ORDERED, bool AXIS, class Fn>
+__device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restrict__ xl4, int k,
+                                           bool valid, const double* xi, float pre_r,
+                                           SweepSmem& sm, Fn& fn) {
     const DomainDev& d = g.dom;
     const int lane = threadIdx.x & 31;
-    uint32_t* qe = smem[threadIdx.x >> 5].e + lane;
+    uint32_t* qe = sm.e + lane;
     int ci[3] = {0, 0, 0};
     AxisOpts ao[3];
 #pragma unroll
@@ -164,9 +164,9 @@ __device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ x
     if (!done) advance();
 
     // When the acceptance radius is <= every cell size, |rel_a| <= |rel| <= R makes
-    // the per-axis cell test redundant for accepted pairs (kernel-uniform flag).
-    // (min_cs is rounded down; the 1e-6 factor covers the rounding of pre_r.)
-    const bool axis_implied = pre_r * 1.000001f <= g.min_cs;
+    // the per-axis cell test redundant for accepted pairs (AXIS = false; chosen
+    // warp-uniformly by sweep() below).
+    constexpr bool axis_implied = !AXIS;
     auto test = [&](const float4 p) {
         const float r0 = fmaf(sg[0], p.x, bq[0]);
         bool rej = !axis_implied && fabsf(r0) > g.lim[0];
@@ -253,6 +253,21 @@ __device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ x
             break;
         }
     }
+}
+
+// Entry point: picks the per-axis-test-free instantiation when every lane's
+// pre-filter radius is below the smallest cell size (min_cs is rounded down; the
+// 1e-6 factor covers the rounding of pre_r), which is the case for every
+// BASELINE deck (radius = cell size / 1.0 or less).
+template <int DIM, bool ORDERED, class Fn>
+__device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ xl4, int k,
+                                      bool valid, const double* xi, float pre_r, Fn&& fn) {
+    __shared__ SweepSmem smem[kSweepThreads / 32];
+    SweepSmem& sm = smem[threadIdx.x >> 5];
+    if (__all_sync(0xffffffffu, !valid || pre_r * 1.000001f <= g.min_cs))
+        sweep_impl<DIM, ORDERED, false>(g, xl4, k, valid, xi, pre_r, sm, fn);
+    else
+        sweep_impl<DIM, ORDERED, true>(g, xl4, k, valid, xi, pre_r, sm, fn);
 }
 
 }  // namespace nau
