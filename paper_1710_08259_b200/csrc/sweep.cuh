@@ -193,12 +193,22 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
     // Process the `steps` oldest entries of every lane (fewer if a lane has fewer).
     auto drain = [&](int steps) {
         __syncwarp();
+        const int took = min(fill, steps);
+        // software pipeline: the next entry's position gather is in flight while
+        // the current pair is evaluated (profiles/r1_v5: the gather's latency was the
+        // top stall of the drain)
+        uint32_t ent_n = took > 0 ? qe[(head & (kQueue - 1)) * 32] : 0u;
+        double4 pj_n = took > 0 ? g.p4[ent_n & ((1u << kSlotBits) - 1)] : make_double4(0, 0, 0, 0);
         for (int s = 0; s < steps; ++s) {
+            const uint32_t ent = ent_n;
+            const double4 pj = pj_n;  // one 32-byte sector per pair
+            if (s + 1 < took) {
+                ent_n = qe[((head + s + 1) & (kQueue - 1)) * 32];
+                pj_n = g.p4[ent_n & ((1u << kSlotBits) - 1)];
+            }
             if (s < fill) {
-                const uint32_t ent = qe[((head + s) & (kQueue - 1)) * 32];
                 const int j = (int)(ent & ((1u << kSlotBits) - 1));
                 const int c = (int)(ent >> kSlotBits);
-                const double4 pj = g.p4[j];  // one 32-byte sector per pair
                 const double xj[3] = {pj.x, pj.y, pj.z};
                 double rel[3] = {0.0, 0.0, 0.0};
                 bool ok = true;
@@ -223,7 +233,6 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
                 if (ok) fn(j, rel, mask);
             }
         }
-        const int took = min(fill, steps);
         head = (head + took) & (kQueue - 1);
         fill -= took;
         __syncwarp();
