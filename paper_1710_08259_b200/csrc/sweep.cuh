@@ -241,7 +241,18 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
     while (true) {
         if (!done) {
             const int stop = min(e, t + kChunk);
-            // four independent loads in flight per lane
+            // eight / four independent loads in flight per lane
+            for (; t + 8 <= stop; t += 8) {
+                float4 p[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) p[u] = xl4[t + u];
+                bool acc[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc[u] = test(p[u]);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (acc[u]) push((uint32_t)(t + u) | icode);
+            }
             for (; t + 4 <= stop; t += 4) {
                 const float4 p0 = xl4[t], p1 = xl4[t + 1], p2 = xl4[t + 2], p3 = xl4[t + 3];
                 const bool a0 = test(p0), a1 = test(p1), a2 = test(p2), a3 = test(p3);
