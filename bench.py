@@ -452,6 +452,73 @@ class Gravity(Workload):
         return {"workload": self.name, "particles": self.sc.n, "pairs_per_step": self.sc.n ** 2}
 
 
+class GravityShard(Gravity):
+    """cfg4 sharded over the ranks: each rank owns N/W bodies (a
+    contiguous block of the global order); positions + masses are all-gathered
+    (NCCL) every step and every rank evaluates its bodies against all sources in
+    global order — identical sums to the single-GPU run."""
+
+    def __init__(self, dist):
+        super().__init__()
+        self.dist = dist
+
+    def setup(self, ctx):
+        import torch
+        from paper_1710_08259_b200 import nau
+        sc, prm = self.sc, self.sc.params
+        W, r = self.dist.world, self.dist.rank
+        N = sc.n
+        assert N % W == 0, "bodies must split evenly for the all-gather"
+        nl = N // W
+        self.g0 = r * nl
+        sl = slice(self.g0, self.g0 + nl)
+        ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+        ctx.set_particles(np.ascontiguousarray(sc.pos[:, sl]))
+        ctx.add_field("v", 3, 1, np.ascontiguousarray(sc.fields["v"][:, sl]))
+        ctx.add_field("a", 3, 1, 0.0)
+        ctx.boundary_shift()
+        self.ctx = ctx
+        self.dev = f"cuda:{torch.cuda.current_device()}"
+        self.local_rows = torch.empty((nl, 4), dtype=torch.float64, device=self.dev)
+        self.all_rows = torch.empty((N, 4), dtype=torch.float64, device=self.dev)
+        self.N, self.nl = N, nl
+        self.fv, self.fa = ctx.fields["v"].id, ctx.fields["a"].id
+        self._forces()  # a(t = 0)
+        self.n_active = nl
+        self.kernels = {107: ("all-pairs gravity", 56.0 * nl, 20.0 * nl * N)}
+        self.h_r = torch.from_numpy(np.ascontiguousarray(sc.pos[:, sl])).pin_memory()
+        self.h_v = torch.from_numpy(np.ascontiguousarray(sc.fields["v"][:, sl])).pin_memory()
+        self.h_out = {k: torch.empty((3, nl), dtype=torch.float64).pin_memory() for k in ("r", "v")}
+        self.h2d = (self.h_r.numel() + self.h_v.numel()) * 8
+        self.d2h = sum(t.numel() for t in self.h_out.values()) * 8
+
+    def _forces(self):
+        import torch
+        ctx, prm = self.ctx, self.sc.params
+        ctx._check(ctx.L.nau_pack_sources(ctx.h, -1, prm["m"], self.local_rows.data_ptr()))
+        if self.dist.world > 1:
+            ctx.sync()
+            self.dist.pg.all_gather_into_tensor(self.all_rows, self.local_rows)
+            torch.cuda.current_stream().synchronize()
+            src = self.all_rows
+        else:
+            src = self.local_rows
+        ctx._check(ctx.L.nau_gravity_sources(ctx.h, src.data_ptr(), self.N, self.g0, prm["G"],
+                                             prm["eps"], self.fa))
+
+    def step(self, ctx):
+        dt = self.sc.params["dt"]
+        ctx.euler(self.fv, self.fa, 0.5 * dt, self.fv)  # v = euler(v, a, dt/2)
+        ctx.euler(0, self.fv, dt, 0)                     # r = euler(r, v, dt) + shift
+        self._forces()                                   # a = nbody_gravity(m, G, eps)
+        ctx.euler(self.fv, self.fa, 0.5 * dt, self.fv)  # v = euler(v, a, dt/2)
+
+    def config(self):
+        c = super().config()
+        c["shards"] = self.dist.world
+        return c
+
+
 class DamBreakSlab(DamBreak):
     """cfg2/cfg0 slab-decomposed along x over the ranks (paper_1710_08259_b200/slab.py):
     each rank owns whole x-cell planes (balanced on particle counts) plus two ghost
@@ -538,6 +605,8 @@ class DamBreakSlab(DamBreak):
 def make_workload(cfg, dist=None, slab=False):
     if slab and cfg in (0, 2):
         return DamBreakSlab(3 if cfg == 2 else 2, dist)
+    if slab and cfg == 4:
+        return GravityShard(dist)
     return {1: Microbench, 2: lambda: DamBreak(3), 0: lambda: DamBreak(2), 3: DemColumn,
             4: Gravity}[cfg]()
 
@@ -566,7 +635,7 @@ def run_ours(args, dist):
     import torch
     from paper_1710_08259_b200 import nau
 
-    use_slab = args.config in (0, 2) and (args.slab or dist.world > 1)
+    use_slab = args.config in (0, 2, 4) and (args.slab or dist.world > 1)
     wl = make_workload(args.config, dist, use_slab)
     ctx = nau.Context(dist.local)
     ctx.set_mode(args.mode == "fast")
@@ -637,7 +706,9 @@ def run_ours(args, dist):
         "scaling": "strong" if use_slab else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": dict(wl.config(), mode=args.mode,
-                       parallelism=(f"x-slabs over {dist.world} GPU(s), NCCL halo+migration"
+                       parallelism=((f"bodies sharded over {dist.world} GPU(s), NCCL all-gather"
+                                     if args.config == 4 else
+                                     f"x-slabs over {dist.world} GPU(s), NCCL halo+migration")
                                     if use_slab else
                                     ("replicas" if dist.world > 1 else "single GPU")),
                        l2="flushed between timed steps (256 MiB memset, untimed)"),

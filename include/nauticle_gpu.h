@@ -206,6 +206,17 @@ typedef struct {
 } nau_gravity_params;
 nau_status nau_leapfrog_step(nau_ctx* ctx, const nau_gravity_params* prm);
 
+/* Sharded n-body: every rank holds a contiguous block of
+ * bodies; the sources are all-gathered each step (NCCL) as (x, y, z, m) rows.
+ * nau_pack_sources writes this rank's rows (m = 0 for inactive bodies; f_m = -1
+ * uses the uniform m) into dev_rows (n x 4 doubles, original order — gravity
+ * never builds cells). nau_gravity_sources: out_field = nbody_gravity(m, G, eps)
+ * of the local bodies against all nsrc sources, skipping source self_off + k for
+ * local body k, summed in global source order (= the single-GPU order). */
+nau_status nau_pack_sources(nau_ctx* ctx, int f_m, double m, double* dev_rows);
+nau_status nau_gravity_sources(nau_ctx* ctx, const double* dev_src, long nsrc, long self_off,
+                               double G, double eps, int out_field);
+
 /* ≙ ReductionNode fsum/fmax/fmin/fmean over active particles (sfl/ast.cpp:237-274).
  * kind: 0 max, 1 min, 2 sum, 3 mean; out has rows*cols doubles (max/min: 1). */
 nau_status nau_reduce(nau_ctx* ctx, int kind, int field_id, double* out);

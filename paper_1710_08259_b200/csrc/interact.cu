@@ -298,6 +298,10 @@ struct GravArgs {
     int has_eps;
     double* out;
     DevErr* err;
+    // external sources (multi-GPU all-gather): (x, y, z, m) rows in global order,
+    // local body k is source self_off + k; m = 0 marks an inactive source
+    const double4* src;
+    long nsrc, self_off;
 };
 
 // FAST: s = G m_j rsqrt(r2)^3 with FMA (≈1e-15 relative per pair); exact: G m_j / (r2 sqrt r2).
@@ -320,9 +324,18 @@ __global__ void __launch_bounds__(kGravTile) k_gravity(const __grid_constant__ G
     const double eps2 = eps * eps;
     double acc[3] = {0.0, 0.0, 0.0};
     bool coincident = false;
-    for (long base = 0; base < n; base += kGravTile) {
+    const long ns = a.src ? a.nsrc : n;
+    const long self = a.self_off + k;
+    for (long base = 0; base < ns; base += kGravTile) {
         const long j = base + threadIdx.x;
-        if (j < n) {
+        if (j < ns && a.src) {
+            const double4 s4 = a.src[j];
+            sx[0][threadIdx.x] = s4.x;
+            if (DIM > 1) sx[1][threadIdx.x] = s4.y;
+            if (DIM > 2) sx[2][threadIdx.x] = s4.z;
+            sm[threadIdx.x] = s4.w;
+            sa[threadIdx.x] = s4.w != 0.0;
+        } else if (j < ns) {
 #pragma unroll
             for (int d = 0; d < DIM; ++d) sx[d][threadIdx.x] = a.x[d * n + j];
             sm[threadIdx.x] = a.m.at(0, (int)j, n);
@@ -334,7 +347,7 @@ __global__ void __launch_bounds__(kGravTile) k_gravity(const __grid_constant__ G
         if (mine && FAST) {
             // branch-free pair loop (FMA via explicit fma(); this TU is -fmad=false):
             // self / inactive pairs are masked, not skipped, so the loop unrolls.
-            const int lim = (int)min((long)kGravTile, n - base);
+            const int lim = (int)min((long)kGravTile, ns - base);
 #pragma unroll 4
             for (int t = 0; t < lim; ++t) {
                 double rel[3] = {0.0, 0.0, 0.0};
@@ -343,7 +356,7 @@ __global__ void __launch_bounds__(kGravTile) k_gravity(const __grid_constant__ G
                 double r2 = eps2;
 #pragma unroll
                 for (int d = DIM - 1; d >= 0; --d) r2 = fma(rel[d], rel[d], r2);
-                const bool ok = (base + t != k) && sa[t];
+                const bool ok = (base + t != self) && sa[t];
                 coincident |= ok && r2 == 0.0;
                 const double inv = rsqrt(ok && r2 > 0.0 ? r2 : 1.0);
                 const double s = ok && r2 > 0.0 ? G * sm[t] * (inv * inv * inv) : 0.0;
@@ -351,9 +364,9 @@ __global__ void __launch_bounds__(kGravTile) k_gravity(const __grid_constant__ G
                 for (int d = 0; d < DIM; ++d) acc[d] = fma(rel[d], s, acc[d]);
             }
         } else if (mine) {
-            const int lim = (int)min((long)kGravTile, n - base);
+            const int lim = (int)min((long)kGravTile, ns - base);
             for (int t = 0; t < lim; ++t) {
-                if (base + t == k || !sa[t]) continue;
+                if (base + t == self || !sa[t]) continue;
                 double rel[3] = {0.0, 0.0, 0.0};
 #pragma unroll
                 for (int d = 0; d < DIM; ++d) rel[d] = sx[d][t] - xi[d];
@@ -429,7 +442,8 @@ void dem_dispatch(nau_ctx* c, int op, const DemArgs& a) {
 }  // namespace
 
 void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int nops, double* out,
-                     int out_rows, int out_cols, int a_rows, int a_cols, const double* gadd) {
+                     int out_rows, int out_cols, int a_rows, int a_cols, const double* gadd,
+                     const GravSources* gsrc) {
     (void)out_rows;
     (void)out_cols;
     if (c->n == 0) return;
@@ -466,6 +480,9 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
         else a.eps = ops[1];
         a.out = out;
         a.err = c->d_err;
+        a.src = gsrc ? gsrc->src : nullptr;
+        a.nsrc = gsrc ? gsrc->nsrc : 0;
+        a.self_off = gsrc ? gsrc->self_off : 0;
         const int blocks = (int)((c->n + kGravTile - 1) / kGravTile);
         prof_begin(c, 100 + op);
         const bool fast = c->mode == NAU_MODE_FAST;

@@ -367,9 +367,13 @@ void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig);
 void launch_unsort(nau_ctx* c, const double* d_src, double* d_dst, int comps);
 void launch_sort_in(nau_ctx* c, const double* d_src_orig, double* d_dst, int comps);
 // interact.cu
+struct GravSources {  // all-gathered (x, y, z, m) rows for sharded n-body
+    const double4* src;
+    long nsrc, self_off;
+};
 void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int nops,
                      double* out, int out_rows, int out_cols, int a_rows, int a_cols,
-                     const double* gadd = nullptr);
+                     const double* gadd = nullptr, const GravSources* gsrc = nullptr);
 // integrate.cu
 void launch_euler(nau_ctx* c, const double* x, const double* xdot, double dt, double* out,
                   int comps);

@@ -120,6 +120,16 @@ __global__ void k_unpack(long m, int width, const double* rows, RowTable t, int 
     active[r] = 1;
 }
 
+__global__ void k_pack_sources(long n, int dim, const double* pos, const uint8_t* active,
+                               const double* mf, double m, double4* out) {
+    const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double x[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < dim; ++a) x[a] = pos[a * n + k];
+    const double mk = active[k] ? (mf ? mf[k] : m) : 0.0;
+    out[k] = make_double4(x[0], x[1], x[2], mk);
+}
+
 RowTable row_table(nau_ctx* c, int* width, int gid_field, int* gid_col) {
     RowTable t{};
     int off = 0;
@@ -186,6 +196,36 @@ nau_status nau_pack_rows(nau_ctx* c, const int* dev_slots, long m, double* dev_r
     nau::RowTable t = nau::row_table(c, &w, -1, nullptr);
     nau::k_pack<<<(int)((m + 255) / 256), 256, 0, c->stream>>>(c->n, dev_slots, m, w, t, dev_rows);
     c->launches++;
+    return NAU_OK;
+}
+
+nau_status nau_pack_sources(nau_ctx* c, int f_m, double m, double* dev_rows) {
+    if (c->fields.empty() || (f_m >= 0 && (f_m >= (int)c->fields.size() || !c->fields[f_m].live)))
+        return NAU_ERR_ARG;
+    if (c->n == 0) return NAU_OK;
+    nau::k_pack_sources<<<(int)((c->n + 255) / 256), 256, 0, c->stream>>>(
+        c->n, c->dom.dim, c->fields[0].d, c->d_active, f_m >= 0 ? c->fields[f_m].d : nullptr, m,
+        reinterpret_cast<double4*>(dev_rows));
+    c->launches++;
+    return NAU_OK;
+}
+
+nau_status nau_gravity_sources(nau_ctx* c, const double* dev_src, long nsrc, long self_off,
+                               double G, double eps, int out_field) {
+    if (c->fields.empty() || out_field <= 0 || out_field >= (int)c->fields.size() ||
+        !c->fields[out_field].live || c->fields[out_field].comps() != c->dom.dim)
+        return NAU_ERR_ARG;
+    nau::Opd ops[3];
+    for (int k = 0; k < 3; ++k) {
+        ops[k].p = nullptr;
+        for (int q = 0; q < 9; ++q) ops[k].v[q] = 0.0;
+    }
+    ops[1].v[0] = G;
+    ops[2].v[0] = eps;
+    nau::GravSources gs{reinterpret_cast<const double4*>(dev_src), nsrc, self_off};
+    const int dim = c->dom.dim;
+    nau::launch_interact(c, NAU_OP_GRAVITY, 0, 0, ops, 3, c->fields[out_field].d, dim, 1, 1, 1,
+                         nullptr, &gs);
     return NAU_OK;
 }
 

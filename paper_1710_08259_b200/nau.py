@@ -38,7 +38,7 @@ EXPORTS = [
     "nau_wcsph_step", "nau_reduce", "nau_sync", "nau_last_error", "nau_profile_enable",
     "nau_profile_ms", "nau_launch_count", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
     "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows", "nau_dem_step",
-    "nau_leapfrog_step",
+    "nau_leapfrog_step", "nau_pack_sources", "nau_gravity_sources",
 ]
 
 
@@ -139,6 +139,8 @@ def load():
         "nau_load_rows": (i, [vp, vp, l, i]),
         "nau_dem_step": (i, [vp, C.POINTER(DemParams)]),
         "nau_leapfrog_step": (i, [vp, C.POINTER(GravityParams)]),
+        "nau_pack_sources": (i, [vp, i, d, vp]),
+        "nau_gravity_sources": (i, [vp, vp, l, l, d, d, i]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

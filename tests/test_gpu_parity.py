@@ -488,3 +488,33 @@ def test_gravity_leapfrog_vs_port(ctx):
     assert rel_err(ctx.download("a"), a) <= TOL_STEP
     mom = ctx.download("v").sum(axis=1) * prm["m"]
     assert np.abs(mom).max() <= 1e-12
+
+
+@pytest.mark.parametrize("fast", [False, True])
+def test_gravity_shard_path_matches_plain(ctx, fast):
+    """The sharded n-body path (pack sources -> [all-gather] -> gravity vs sources) on one
+    rank = the plain leapfrog, bitwise (same global source order)."""
+    import bench
+
+    class D:
+        world, rank, local, pg = 1, 0, 0, None
+
+    plain = bench.Gravity.__new__(bench.Gravity)
+    plain.sc = scenes.plummer(n=2048)
+    ctx.set_mode(fast)
+    plain.setup(ctx)
+    for _ in range(3):
+        plain.step(ctx)
+    ref = {k: ctx.download(k) for k in ("r", "v", "a")}
+    ctx2 = nau.Context(0)
+    ctx2.set_mode(fast)
+    sh = bench.GravityShard.__new__(bench.GravityShard)
+    sh.dist = D()
+    sh.sc = scenes.plummer(n=2048)
+    sh.setup(ctx2)
+    for _ in range(3):
+        sh.step(ctx2)
+    for k in ("r", "v", "a"):
+        np.testing.assert_array_equal(ctx2.download(k), ref[k], err_msg=k)
+    ctx.set_mode(False)
+    ctx2.close()
