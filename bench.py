@@ -602,11 +602,74 @@ class DamBreakSlab(DamBreak):
         return c
 
 
+class DemSlab(DemColumn):
+    """cfg3 slab-decomposed along x (0.3 m ≈ 85 planes, balanced while
+    the column settles in z); same slab driver as the dam break, DEM deck step."""
+
+    FIELDS = ["v", "vdot", "R", "m"]
+
+    def __init__(self, dist):
+        super().__init__()
+        self.dist = dist
+
+    def setup(self, ctx):
+        import torch
+        from paper_1710_08259_b200 import nau, slab
+        sc, prm = self.sc, self.sc.params
+        ncx = sc.max_cells[0] - sc.min_cells[0]
+        cx = slab.cell_x_of(sc.pos[0], 0.0, sc.cell_size[0], ncx, False)
+        world, rank = self.dist.world, self.dist.rank
+        self.bounds = slab.balanced_bounds(cx, ncx, world)
+        rows = slab.initial_rows(sc, self.FIELDS, self.bounds, rank, ncx, False)
+        ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+        ctx.set_particles(np.ascontiguousarray(rows[:, :3].T))
+        col = 3
+        for k in self.FIELDS + ["gid", "ghost"]:
+            w = 3 if k in ("v", "vdot") else 1
+            ctx.add_field(k, w, 1, np.ascontiguousarray(rows[:, col:col + w].T))
+            col += w
+        ctx.boundary_shift()
+        ctx.build_cells()
+        p = nau.DemParams()
+        f = ctx.fields
+        p.law, p.f_v, p.f_vdot, p.f_R, p.f_m = 8, f["v"].id, f["vdot"].id, f["R"].id, f["m"].id
+        p.P, p.Q, p.cf, p.search_radius, p.dt = prm["kn"], prm["en"], prm["cf"], \
+            prm["search_radius"], prm["dt"]
+        for a in range(3):
+            p.g[a] = prm["g"][a]
+        self.p = p
+        self.backend = slab.GpuBackend(ctx, lambda: ctx.dem_step(p), self.FIELDS)
+        ex = slab.Exchanger(self.dist.pg, rank, world, False, self.backend.device)
+        self.rank_drv = slab.SlabRank(self.backend, ex, self.bounds, ncx, False)
+        self.n_active = int((rows[:, -1] == 0).sum())
+        N = float(len(rows))
+        self.kernels = {108: ("dem_lsd contact sum", 88.0 * N, 0.0),
+                        301: ("symplectic integrator", 8.0 * 22 * N, 20.0 * N),
+                        300: ("cell build", (24.0 + 8 + 60 + 4 + 16 * 13) * N, 0.0)}
+        self.cand_per_particle = float("nan")
+        self.h_rows = torch.from_numpy(rows).pin_memory()
+        self.h_out = torch.empty_like(self.h_rows).pin_memory()
+        self.h2d = self.d2h = self.h_rows.numel() * 8
+
+    def step(self, ctx):
+        self.rank_drv.step()
+
+    def e2e_step(self, ctx):
+        DamBreakSlab.e2e_step(self, ctx)
+
+    def config(self):
+        sc = self.sc
+        return {"workload": self.name, "particles": sc.n, "dt": sc.params["dt"],
+                "slabs": self.bounds, "ghost_planes": 2}
+
+
 def make_workload(cfg, dist=None, slab=False):
     if slab and cfg in (0, 2):
         return DamBreakSlab(3 if cfg == 2 else 2, dist)
     if slab and cfg == 4:
         return GravityShard(dist)
+    if slab and cfg == 3:
+        return DemSlab(dist)
     return {1: Microbench, 2: lambda: DamBreak(3), 0: lambda: DamBreak(2), 3: DemColumn,
             4: Gravity}[cfg]()
 
@@ -635,7 +698,7 @@ def run_ours(args, dist):
     import torch
     from paper_1710_08259_b200 import nau
 
-    use_slab = args.config in (0, 2, 4) and (args.slab or dist.world > 1)
+    use_slab = args.config in (0, 2, 3, 4) and (args.slab or dist.world > 1)
     wl = make_workload(args.config, dist, use_slab)
     ctx = nau.Context(dist.local)
     ctx.set_mode(args.mode == "fast")

@@ -332,6 +332,7 @@ void nau_destroy(nau_ctx* c) {
     free_cells(c);
     dfree(c->d_err);
     dfree(c->d_red);
+    dfree(c->d_sel);
     if (c->h_err) cudaFreeHost(c->h_err);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -329,6 +329,8 @@ struct nau_ctx {
     float4* d_xl = nullptr;  // fp32 global-origin coordinates (sweep pre-filters)
     double4* d_aux = nullptr;  // per-particle scratch (fast WCSPH: v and p / rho^2 packed)
     double4* d_p4 = nullptr;  // packed positions (written by the reorder pass)
+    int* d_sel = nullptr;     // nau_select block-count scratch
+    long sel_len = 0;
     int mode = NAU_MODE_EXACT;
     int* d_cell_start = nullptr;  // ncells + 2
     int* d_cell_count = nullptr;  // ncells + 1

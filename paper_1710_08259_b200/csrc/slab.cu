@@ -171,8 +171,12 @@ nau_status nau_select(nau_ctx* c, int axis, double lo, double hi, int flag_field
     const long n = c->n;
     if (n == 0) return NAU_OK;
     const int nb = (int)((n + nau::kSelBlock - 1) / nau::kSelBlock);
-    int* scratch = nullptr;
-    if (cudaMalloc(&scratch, sizeof(int) * (nb + 1)) != cudaSuccess) return NAU_ERR_CUDA;
+    if (c->sel_len < nb + 1) {  // context-owned scratch: no per-call malloc/free (cudaFree syncs)
+        if (c->d_sel) cudaFree(c->d_sel);
+        c->sel_len = 2L * (nb + 1);
+        if (cudaMalloc(&c->d_sel, sizeof(int) * c->sel_len) != cudaSuccess) return NAU_ERR_CUDA;
+    }
+    int* scratch = c->d_sel;
     const double* flag = flag_field >= 0 ? c->fields[flag_field].d : nullptr;
     const double* pos = c->fields[0].d;
     nau::k_sel_count<<<nb, nau::kSelBlock, 0, c->stream>>>(c->dom, pos, c->d_active, n, axis, lo, hi, flag,
@@ -184,7 +188,6 @@ nau_status nau_select(nau_ctx* c, int axis, double lo, double hi, int flag_field
     int total = 0;
     cudaMemcpyAsync(&total, scratch + nb, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
     cudaError_t e = cudaStreamSynchronize(c->stream);
-    cudaFree(scratch);
     if (e != cudaSuccess) return NAU_ERR_CUDA;
     *count = total;
     return NAU_OK;

@@ -243,4 +243,7 @@ class GpuBackend:
         return self.torch.cat(blocks, 0)
 
     def step(self):
-        self.ctx.wcsph_step(self.p)
+        if callable(self.p):
+            self.p()  # a deck step callback (e.g. the DEM deck)
+        else:
+            self.ctx.wcsph_step(self.p)
