@@ -97,6 +97,10 @@ void nau_destroy(nau_ctx* ctx);
 enum { NAU_MODE_EXACT = 0, NAU_MODE_FAST = 1 };
 nau_status nau_set_mode(nau_ctx* ctx, int mode);
 int nau_get_mode(nau_ctx* ctx);
+/* Per-step neighbour lists for nau_wcsph_step (default on): the cell sweep runs
+ * once per step and both passes read its list; same candidates in the same
+ * order, so results are identical either way. Off = each pass sweeps itself. */
+nau_status nau_set_neighbor_lists(nau_ctx* ctx, int on);
 /* Use an external CUDA stream (cudaStream_t), e.g. torch's current stream. NULL = own stream. */
 nau_status nau_set_stream(nau_ctx* ctx, void* stream);
 void* nau_get_stream(nau_ctx* ctx);

@@ -333,6 +333,9 @@ void nau_destroy(nau_ctx* c) {
     dfree(c->d_err);
     dfree(c->d_red);
     dfree(c->d_sel);
+    dfree(c->d_nlist);
+    dfree(c->d_ncount);
+    dfree(c->d_nover);
     if (c->h_err) cudaFreeHost(c->h_err);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -714,12 +717,14 @@ nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
         nau_status s = nau_build_cells(c);
         if (s != NAU_OK) return s;
     }
+    // Both passes of the step share one neighbour list (same candidates, same order).
+    const bool lists = nau::build_nlist(c, p->radius, c->mode == NAU_MODE_EXACT);
     if (c->mode == NAU_MODE_FAST) {
-        nau::launch_wcsph_fast(c, p, c->d_aux);
+        nau::launch_wcsph_fast(c, p, c->d_aux, lists);
         nau::launch_symplectic(c, c->fields[p->f_v].d, c->fields[p->f_vdot].d,
                                p->f_mask >= 0 ? c->fields[p->f_mask].d : nullptr, p->dt);
     } else {
-        nau::launch_wcsph(c, p);
+        nau::launch_wcsph(c, p, lists);
     }
     c->dirty = true;
     return NAU_OK;
@@ -783,6 +788,11 @@ nau_status nau_set_mode(nau_ctx* c, int mode) {
 }
 
 int nau_get_mode(nau_ctx* c) { return c->mode; }
+
+nau_status nau_set_neighbor_lists(nau_ctx* c, int on) {
+    c->use_nlist = on != 0;
+    return NAU_OK;
+}
 
 nau_status nau_reduce(nau_ctx* c, int kind, int id, double* out) {
     if (!field_ok(c, id) || kind < 0 || kind > 3) return fail(c, NAU_ERR_ARG, "bad reduce args");

@@ -220,6 +220,23 @@ __global__ void __launch_bounds__(kSweepThreads) k_neighbor_counts(Geo g, const 
     if (valid) out[g.orig[k]] = cnt;
 }
 
+// Neighbour lists: the sweep's scan phase alone, survivors written to the
+// lane-interleaved list (sweep.cuh build_list). Per-lane loop, no warp votes.
+template <int DIM, bool ORDERED>
+__global__ void __launch_bounds__(kSweepThreads) k_nlist(const __grid_constant__ Geo g,
+                                                         const float4* xl, float pre_r,
+                                                         uint32_t* list, int* count, int cap,
+                                                         int* over) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= *g.nact) return;
+    uint32_t* lst = list + nlist_base(k, cap);
+    const int cnt = pre_r * 1.000001f <= g.min_cs
+                        ? build_list<DIM, ORDERED, false>(g, xl, k, pre_r, lst, cap)
+                        : build_list<DIM, ORDERED, true>(g, xl, k, pre_r, lst, cap);
+    count[k] = min(cnt, cap);
+    if (cnt > cap) atomicMax(over, cnt);
+}
+
 __global__ void k_unsort(long n, int comps, const int* orig, const double* src, double* dst) {
     long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -305,6 +322,63 @@ void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig) {
         default: k_neighbor_counts<3><<<b, T, 0, c->stream>>>(g, c->d_xl, radius, d_out_orig); break;
     }
     c->launches++;
+}
+
+bool build_nlist(nau_ctx* c, double radius, bool ordered) {
+    const long n = c->n;
+    if (n == 0 || !c->use_nlist) return false;
+    constexpr int kMaxCap = 4096;  // beyond this the lists would cost more than they save
+    const size_t slots = (size_t)((n + 31) / 32) * 32;
+    if (c->nl_cap == 0) c->nl_cap = 64;
+    if (!c->d_nover && cudaMalloc(&c->d_nover, sizeof(int)) != cudaSuccess) return false;
+    if (c->nc_len < n) {
+        if (c->d_ncount) cudaFree(c->d_ncount);
+        c->d_ncount = nullptr;
+        c->nc_len = 0;
+        if (cudaMalloc(&c->d_ncount, sizeof(int) * slots) != cudaSuccess) return false;
+        c->nc_len = (long)slots;
+    }
+    Geo g = make_geo(c);
+    const int T = kSweepThreads;
+    const int b = blocks_for(n, T);
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        const size_t need = slots * (size_t)c->nl_cap;
+        if (c->nl_len < need) {
+            if (c->d_nlist) cudaFree(c->d_nlist);
+            c->d_nlist = nullptr;
+            c->nl_len = 0;
+            if (cudaMalloc(&c->d_nlist, sizeof(uint32_t) * need) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            c->nl_len = need;
+        }
+        cudaMemsetAsync(c->d_nover, 0, sizeof(int), c->stream);
+        const float r = (float)radius;
+        prof_begin(c, 302);
+        if (ordered) {
+            switch (c->dom.dim) {
+                case 1: k_nlist<1, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
+                case 2: k_nlist<2, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
+                default: k_nlist<3, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
+            }
+        } else {
+            switch (c->dom.dim) {
+                case 1: k_nlist<1, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
+                case 2: k_nlist<2, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
+                default: k_nlist<3, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
+            }
+        }
+        prof_end(c, 302);
+        c->launches++;
+        int over = 0;
+        cudaMemcpyAsync(&over, c->d_nover, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+        if (cudaStreamSynchronize(c->stream) != cudaSuccess) return false;
+        if (over == 0) return true;
+        if (over > kMaxCap) return false;
+        c->nl_cap = std::min(kMaxCap, ((over + over / 4 + 31) / 32) * 32);
+    }
+    return false;
 }
 
 void launch_unsort(nau_ctx* c, const double* d_src, double* d_dst, int comps) {

@@ -95,11 +95,12 @@ struct WcsphArgs {
     const double* v;
     double* vdot;
     DevErr* err;
+    NList nl;
 };
 
 // Pass 1: rho = sph_S(one, m, one, K, R) (interactions.cpp:40-58 with A = rho = 1),
 //         p = B*((rho/rho0)^gamma - 1).
-template <int DIM, int KF>
+template <int DIM, int KF, bool LIST>
 __global__ void __launch_bounds__(kThreads) k_wcsph_density(const __grid_constant__ WcsphArgs a) {
     const Geo& g = a.g;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(kThreads) k_wcsph_density(const __grid_constan
     const double alpha = kernel_alpha<KF>(a.kdim, h);
     const double s_unit = a.mass / 1.0;  // m_j / rho_j with the uniform operand rho = 1
     double acc = 0.0;
-    sweep<DIM, true>(g, a.xl, k, valid, xi, (float)radius,
+    for_neighbors<DIM, true, LIST>(g, a.xl, a.nl, k, valid, xi, (float)radius,
                [&](int, const double* rel, int) {
         const double dist = norm_rel<DIM>(rel);
         if (dist > radius) return;
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(kThreads) k_wcsph_density(const __grid_constan
 
 // Pass 2: vdot = -1/rho*sph_G11(p,m,rho,K,R) + visc*sph_A(v,m,rho,K,R) + g, one
 // neighbour walk with the two operators' accumulators kept apart.
-template <int DIM, int KF>
+template <int DIM, int KF, bool LIST>
 __global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_constant__ WcsphArgs a) {
     const Geo& g = a.g;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_consta
     }
     const double pr_i = p_i / (rho_i * rho_i);
     double G[3] = {0.0, 0.0, 0.0}, A[3] = {0.0, 0.0, 0.0};
-    sweep<DIM, true>(g, a.xl, k, valid, xi, (float)radius,
+    for_neighbors<DIM, true, LIST>(g, a.xl, a.nl, k, valid, xi, (float)radius,
                [&](int j, const double* rel, int mask) {
         const double dist = norm_rel<DIM>(rel);
         if (dist > radius) return;
@@ -240,24 +241,32 @@ __global__ void k_reduce_partial(long n, int comps, int kind, const uint8_t* act
         for (int c = 0; c < 9; ++c) part[blockIdx.x * 9 + c] = sh[0][c];
 }
 
-template <int DIM>
+template <int DIM, bool LIST>
 void wcsph_launch(nau_ctx* c, const WcsphArgs& a, int kf) {
     const int blocks = (int)((c->n + kThreads - 1) / kThreads);
     prof_begin(c, 200);
     if (kf == NAU_K_CUBIC) {
-        k_wcsph_density<DIM, NAU_K_CUBIC><<<blocks, kThreads, 0, c->stream>>>(a);
+        k_wcsph_density<DIM, NAU_K_CUBIC, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
     } else {
-        k_wcsph_density<DIM, NAU_K_WENDLAND><<<blocks, kThreads, 0, c->stream>>>(a);
+        k_wcsph_density<DIM, NAU_K_WENDLAND, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
     }
     prof_end(c, 200);
     prof_begin(c, 201);
     if (kf == NAU_K_CUBIC) {
-        k_wcsph_momentum<DIM, NAU_K_CUBIC><<<blocks, kThreads, 0, c->stream>>>(a);
+        k_wcsph_momentum<DIM, NAU_K_CUBIC, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
     } else {
-        k_wcsph_momentum<DIM, NAU_K_WENDLAND><<<blocks, kThreads, 0, c->stream>>>(a);
+        k_wcsph_momentum<DIM, NAU_K_WENDLAND, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
     }
     prof_end(c, 201);
     c->launches += 2;
+}
+
+template <int DIM>
+void wcsph_launch_dim(nau_ctx* c, const WcsphArgs& a, int kf) {
+    if (a.nl.e)
+        wcsph_launch<DIM, true>(c, a, kf);
+    else
+        wcsph_launch<DIM, false>(c, a, kf);
 }
 
 }  // namespace
@@ -280,9 +289,10 @@ void launch_symplectic(nau_ctx* c, double* v, const double* vdot, const double* 
     c->launches++;
 }
 
-void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p) {
+void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p, bool lists) {
     if (c->n == 0) return;
     WcsphArgs a;
+    a.nl = NList{lists ? c->d_nlist : nullptr, c->d_ncount, c->nl_cap};
     a.g = make_geo(c);
     a.xl = c->d_xl;
     a.mass = p->mass;
@@ -299,9 +309,9 @@ void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p) {
     a.vdot = c->fields[p->f_vdot].d;
     a.err = c->d_err;
     switch (c->dom.dim) {
-        case 1: wcsph_launch<1>(c, a, p->kernel_family); break;
-        case 2: wcsph_launch<2>(c, a, p->kernel_family); break;
-        default: wcsph_launch<3>(c, a, p->kernel_family); break;
+        case 1: wcsph_launch_dim<1>(c, a, p->kernel_family); break;
+        case 2: wcsph_launch_dim<2>(c, a, p->kernel_family); break;
+        default: wcsph_launch_dim<3>(c, a, p->kernel_family); break;
     }
     const double* mask = p->f_mask >= 0 ? c->fields[p->f_mask].d : nullptr;
     launch_symplectic(c, c->fields[p->f_v].d, c->fields[p->f_vdot].d, mask, p->dt);

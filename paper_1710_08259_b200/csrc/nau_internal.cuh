@@ -331,6 +331,15 @@ struct nau_ctx {
     double4* d_p4 = nullptr;  // packed positions (written by the reorder pass)
     int* d_sel = nullptr;     // nau_select block-count scratch
     long sel_len = 0;
+    // per-step neighbour lists of the WCSPH deck (k_nlist): cap entries per slot,
+    // grown on overflow; lists off => every pass sweeps the cells itself
+    bool use_nlist = true;
+    uint32_t* d_nlist = nullptr;
+    size_t nl_len = 0;   // entries allocated
+    int* d_ncount = nullptr;
+    long nc_len = 0;
+    int* d_nover = nullptr;  // max list length seen when > cap (0 = fits)
+    int nl_cap = 0;
     int mode = NAU_MODE_EXACT;
     int* d_cell_start = nullptr;  // ncells + 2
     int* d_cell_count = nullptr;  // ncells + 1
@@ -366,6 +375,7 @@ void prof_end(nau_ctx* c, int cls);
 void launch_boundary_shift(nau_ctx* c);
 void launch_build_cells(nau_ctx* c);
 void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig);
+bool build_nlist(nau_ctx* c, double radius, bool ordered);  // false: lists unusable this step
 void launch_unsort(nau_ctx* c, const double* d_src, double* d_dst, int comps);
 void launch_sort_in(nau_ctx* c, const double* d_src_orig, double* d_dst, int comps);
 // interact.cu
@@ -380,11 +390,11 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
 void launch_euler(nau_ctx* c, const double* x, const double* xdot, double dt, double* out,
                   int comps);
 void launch_symplectic(nau_ctx* c, double* v, const double* vdot, const double* mask, double dt);
-void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p);
+void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p, bool lists);
 void launch_reduce(nau_ctx* c, int kind, const double* f, int comps, double* h_out);
 // fast.cu
 bool fast_supports(int op, int a_rows, int a_cols, int dim);
 void launch_interact_fast(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, double* out,
                           int a_rows);
-void launch_wcsph_fast(nau_ctx* c, const nau_wcsph_params* p, double4* vp);
+void launch_wcsph_fast(nau_ctx* c, const nau_wcsph_params* p, double4* vp, bool lists);
 }  // namespace nau

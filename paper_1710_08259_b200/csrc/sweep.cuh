@@ -275,6 +275,129 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
     }
 }
 
+// ---- per-step neighbour lists (used by the two-pass WCSPH deck) --------------
+// The density and momentum passes of a step walk the same candidates, so the
+// scan phase runs once (k_nlist) and stores every pre-filter survivor, in
+// candidate order, into a lane-interleaved list: entry s of slot k lives at
+// list[((k/32)*cap + s)*32 + k%32] (coalesced for a warp). The passes then only
+// consume their list (consume_list). Same order as the sweep => same sums.
+template <int DIM, bool ORDERED, bool AXIS>
+__device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict__ xl4, int k,
+                                          float pre_r, uint32_t* lst, int cap) {
+    const DomainDev& d = g.dom;
+    int ci[3] = {0, 0, 0};
+    decode_cell<DIM>(d, g.key[k], ci);
+    AxisOpts ao[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ao[a] = AxisOpts{0, 1, 1};
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) ao[a] = axis_opts(d, a, ci[a]);
+    const float4 pi = xl4[k];
+    const float xli[3] = {pi.x, pi.y, pi.z};
+    const float rl = pre_r * 1.001f + g.pre_abs;
+    const float r2lim = rl * rl;
+    const int n01 = ao[0].cnt * (DIM > 1 ? ao[1].cnt : 1);
+    const int ncombo = n01 * (DIM > 2 ? ao[2].cnt : 1);
+    int cnt = 0;
+    for (int idx = 0; idx < ncombo; ++idx) {
+        const int combo = ORDERED ? idx : ((idx & 1) ? ncombo - 1 - (idx >> 1) : (idx >> 1));
+        const int o0 = combo % ao[0].cnt;
+        const int o1 = DIM > 1 ? (combo / ao[0].cnt) % ao[1].cnt : 0;
+        const int o2 = DIM > 2 ? combo / n01 : 0;
+        int cell, ic, flat, code;
+        float sg[3] = {1.f, 1.f, 1.f}, bq[3] = {0.f, 0.f, 0.f}, bs;
+        option_of(d, 0, ci[0], ao[0], o0, cell, ic, sg[0], bs);
+        flat = cell;
+        code = ic;
+        bq[0] = bs - xli[0];
+        if (DIM > 1) {
+            option_of(d, 1, ci[1], ao[1], o1, cell, ic, sg[1], bs);
+            flat += d.cells[0] * cell;
+            code += 5 * ic;
+            bq[1] = bs - xli[1];
+        }
+        if (DIM > 2) {
+            option_of(d, 2, ci[2], ao[2], o2, cell, ic, sg[2], bs);
+            flat += d.cells[0] * d.cells[1] * cell;
+            code += 25 * ic;
+            bq[2] = bs - xli[2];
+        }
+        const uint32_t icode = (uint32_t)code << kSlotBits;
+        const int s = g.cell_start[flat], e = s + g.cell_count[flat];
+        auto test = [&](const float4 p) {
+            const float r0 = fmaf(sg[0], p.x, bq[0]);
+            bool rej = AXIS && fabsf(r0) > g.lim[0];
+            float r2 = r0 * r0;
+            if (DIM > 1) {
+                const float r1 = fmaf(sg[1], p.y, bq[1]);
+                rej |= AXIS && fabsf(r1) > g.lim[1];
+                r2 = fmaf(r1, r1, r2);
+            }
+            if (DIM > 2) {
+                const float r3 = fmaf(sg[2], p.z, bq[2]);
+                rej |= AXIS && fabsf(r3) > g.lim[2];
+                r2 = fmaf(r3, r3, r2);
+            }
+            return !(rej || r2 > r2lim);
+        };
+        int t = s;
+        for (; t + 4 <= e; t += 4) {
+            const float4 p0 = xl4[t], p1 = xl4[t + 1], p2 = xl4[t + 2], p3 = xl4[t + 3];
+            const bool a0 = test(p0), a1 = test(p1), a2 = test(p2), a3 = test(p3);
+            if (a0) { if (cnt < cap) lst[cnt * 32] = (uint32_t)t | icode; ++cnt; }
+            if (a1) { if (cnt < cap) lst[cnt * 32] = (uint32_t)(t + 1) | icode; ++cnt; }
+            if (a2) { if (cnt < cap) lst[cnt * 32] = (uint32_t)(t + 2) | icode; ++cnt; }
+            if (a3) { if (cnt < cap) lst[cnt * 32] = (uint32_t)(t + 3) | icode; ++cnt; }
+        }
+        for (; t < e; ++t)
+            if (test(xl4[t])) {
+                if (cnt < cap) lst[cnt * 32] = (uint32_t)t | icode;
+                ++cnt;
+            }
+    }
+    return cnt;
+}
+
+// Evaluate fn over a slot's list (lane-private loop; the next gather is in flight
+// while the current pair is evaluated).
+template <int DIM, bool AXIS, class Fn>
+__device__ __forceinline__ void consume_list(const Geo& g, const uint32_t* __restrict__ lst, int cnt,
+                                             const double* xi, Fn&& fn) {
+    uint32_t ent_n = cnt > 0 ? lst[0] : 0u;
+    double4 pj_n = cnt > 0 ? g.p4[ent_n & ((1u << kSlotBits) - 1)] : make_double4(0, 0, 0, 0);
+    for (int s = 0; s < cnt; ++s) {
+        const uint32_t ent = ent_n;
+        const double4 pj = pj_n;
+        if (s + 1 < cnt) {
+            ent_n = lst[(s + 1) * 32];
+            pj_n = g.p4[ent_n & ((1u << kSlotBits) - 1)];
+        }
+        const int j = (int)(ent & ((1u << kSlotBits) - 1));
+        const int c = (int)(ent >> kSlotBits);
+        const double xj[3] = {pj.x, pj.y, pj.z};
+        double rel[3] = {0.0, 0.0, 0.0};
+        bool ok = true;
+        int mask = 0;
+        if (c == 0) {
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                rel[a] = (xj[a] + 0.0) - xi[a];
+                ok &= !AXIS || !(fabs(rel[a]) > g.img[a].cs);
+            }
+        } else {
+            const int cc[3] = {c % 5, (c / 5) % 5, c / 25};
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                const double r = image_of(g.img[a], xj[a], cc[a]) - xi[a];
+                ok &= !AXIS || !(fabs(r) > g.img[a].cs);
+                rel[a] = r;
+                mask |= (cc[a] >= 3) << a;
+            }
+        }
+        if (ok) fn(j, rel, mask);
+    }
+}
+
 // Entry point: picks the per-axis-test-free instantiation when every lane's
 // pre-filter radius is below the smallest cell size (min_cs is rounded down; the
 // 1e-6 factor covers the rounding of pre_r), which is the case for every
@@ -288,6 +411,35 @@ __device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ x
         sweep_impl<DIM, ORDERED, false>(g, xl4, k, valid, xi, pre_r, sm, fn);
     else
         sweep_impl<DIM, ORDERED, true>(g, xl4, k, valid, xi, pre_r, sm, fn);
+}
+
+struct NList {  // per-step neighbour lists (k_nlist in cells.cu)
+    const uint32_t* e;
+    const int* count;
+    int cap;
+};
+
+__device__ __forceinline__ size_t nlist_base(int k, int cap) {
+    return (size_t)(k >> 5) * cap * 32 + (k & 31);
+}
+
+// fn over k's neighbour candidates: from the step's list (LIST) or a fresh sweep.
+// Both visit the same candidates in the same order.
+template <int DIM, bool ORDERED, bool LIST, class Fn>
+__device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __restrict__ xl4,
+                                              const NList& nl, int k, bool valid,
+                                              const double* xi, float pre_r, Fn&& fn) {
+    if constexpr (LIST) {
+        if (!valid) return;
+        const uint32_t* lst = nl.e + nlist_base(k, nl.cap);
+        const int cnt = nl.count[k];
+        if (pre_r * 1.000001f <= g.min_cs)
+            consume_list<DIM, false>(g, lst, cnt, xi, fn);
+        else
+            consume_list<DIM, true>(g, lst, cnt, xi, fn);
+    } else {
+        sweep<DIM, ORDERED>(g, xl4, k, valid, xi, pre_r, fn);
+    }
 }
 
 }  // namespace nau

@@ -38,7 +38,7 @@ EXPORTS = [
     "nau_wcsph_step", "nau_reduce", "nau_sync", "nau_last_error", "nau_profile_enable",
     "nau_profile_ms", "nau_launch_count", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
     "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows", "nau_dem_step",
-    "nau_leapfrog_step", "nau_pack_sources", "nau_gravity_sources",
+    "nau_leapfrog_step", "nau_pack_sources", "nau_gravity_sources", "nau_set_neighbor_lists",
 ]
 
 
@@ -141,6 +141,7 @@ def load():
         "nau_leapfrog_step": (i, [vp, C.POINTER(GravityParams)]),
         "nau_pack_sources": (i, [vp, i, d, vp]),
         "nau_gravity_sources": (i, [vp, vp, l, l, d, d, i]),
+        "nau_set_neighbor_lists": (i, [vp, i]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -226,6 +227,10 @@ class Context:
     @property
     def fast(self):
         return self.L.nau_get_mode(self.h) == MODE_FAST
+
+    def set_neighbor_lists(self, on: bool):
+        """Per-step neighbour lists for wcsph_step (identical results, faster)."""
+        self._check(self.L.nau_set_neighbor_lists(self.h, 1 if on else 0))
 
     def set_stream(self, stream_ptr):
         self._check(self.L.nau_set_stream(self.h, C.c_void_p(stream_ptr)))

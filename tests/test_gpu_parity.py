@@ -338,6 +338,70 @@ def test_fast_mode_dam_break_vs_port(ctx):
     np.testing.assert_array_equal(ctx.active(), ps.active)
 
 
+# ------------------------------------------------------- neighbour lists ----
+def _run_deck(build, fast, lists, steps):
+    c = nau.Context(0)
+    try:
+        p = build(c)
+        c.set_mode(fast)
+        c.set_neighbor_lists(lists)
+        for _ in range(steps):
+            c.wcsph_step(p)
+        return {k: c.download(k) for k in ("r", "rho", "p", "v", "vdot")}, c.active()
+    finally:
+        c.close()
+
+
+def _random_deck(n, seed, kind, radius):
+    """n random particles in the unit square, 4 x 4 cells of 0.25 (lists of up
+    to ~n pi radius^2 entries: exercises the list capacity growth/fallback)."""
+    def build(c):
+        rng = np.random.default_rng(seed)
+        c.set_domain(2, [0, 0], [4, 4], [0.25, 0.25], [kind, kind])
+        c.set_particles(rng.random((2, n)))
+        c.add_field("rho", 1, 1, 0.0)
+        c.add_field("p", 1, 1, 0.0)
+        c.add_field("v", 2, 1, 0.01 * rng.standard_normal((2, n)))
+        c.add_field("vdot", 2, 1, 0.0)
+        c.add_field("mask", 1, 1, 1.0)
+        p = nau.WcsphParams()
+        p.kernel_family, p.kernel_dim = nau.K_WENDLAND, 2
+        p.mass, p.radius, p.rho0, p.B = 1.0 / n, radius, 1.0, 1.0
+        p.gamma, p.visc, p.dt = 7.0, 0.1, 1e-4
+        p.g[1] = -1.0
+        f = c.fields
+        p.f_rho, p.f_p, p.f_v, p.f_vdot, p.f_mask = (f["rho"].id, f["p"].id, f["v"].id,
+                                                     f["vdot"].id, f["mask"].id)
+        return p
+    return build
+
+
+@pytest.mark.parametrize("fast", [False, True])
+def test_neighbor_lists_identical_to_sweep_dam3d(fast):
+    """The per-step lists visit the sweep's candidates in the sweep's order: bitwise
+    identical results with lists on and off (3D dam break, both modes)."""
+    build = lambda c: _gpu_dam(c, scenes.dam_break(3, dx=0.02))
+    on, act_on = _run_deck(build, fast, True, 3)
+    off, act_off = _run_deck(build, fast, False, 3)
+    np.testing.assert_array_equal(act_on, act_off)
+    for k in on:
+        np.testing.assert_array_equal(on[k], off[k], err_msg=k)
+
+
+@pytest.mark.parametrize("n,radius,kind", [(8000, 0.25, nau.PERIODIC),
+                                           (8000, 0.25, nau.SYMMETRIC),
+                                           (24000, 0.25, nau.PERIODIC)])
+def test_neighbor_lists_capacity_growth_and_fallback(n, radius, kind):
+    """~1600 entries per list (capacity grows from 64 in one retry) and ~4700 (above
+    the list cap: the step falls back to sweeping) give the sweep's results."""
+    build = _random_deck(n, 77, kind, radius)
+    for fast in (False, True):
+        on, _ = _run_deck(build, fast, True, 2)
+        off, _ = _run_deck(build, fast, False, 2)
+        for k in on:
+            np.testing.assert_array_equal(on[k], off[k], err_msg=(fast, k))
+
+
 # ------------------------------------------------------- slab primitives ----
 def test_select_pack_load_roundtrip(ctx):
     import torch
