@@ -240,9 +240,9 @@ class Microbench(Workload):
         N = float(sc.n)
         # per-particle bytes / flops
         self.kernels = {
-            100: ("sph_S density", 32.0 * N, 8 * C + 14 * nn),
-            102: ("sph_G11 gradient", 64.0 * N, 8 * C + 24 * nn),
-            103: ("sph_L0 Laplacian", 48.0 * N, 8 * C + 27 * nn),
+            100: ("sph_S density", 32.0 * N, 14 * nn),
+            102: ("sph_G11 gradient", 64.0 * N, 24 * nn),
+            103: ("sph_L0 Laplacian", 48.0 * N, 27 * nn),
             300: ("cell build", (32.0 + 60.0 + 4.0 + 16.0 * 8) * N, 0.0),
         }
         self.cand_per_particle = C / N
@@ -315,8 +315,9 @@ class DamBreak(Workload):
         d = sc.dim
         self.n_active = sc.n
         self.kernels = {
-            200: ("density+EOS", (8.0 * d + 8 + 8) * N, 8 * C + 14 * nn + 10 * N),
-            201: ("momentum G11+A", (8.0 * d * 3 + 16) * N, 8 * C + 42 * nn),
+            200: ("density+EOS", (8.0 * d + 8 + 8) * N, 14 * nn + 10 * N),
+            201: ("momentum G11+A", (8.0 * d * 3 + 16) * N, 42 * nn),
+            302: ("neighbour-list build", 20.0 * N + 4.0 * nn, 0.0),
             301: ("symplectic integrator", (8.0 * (4 * d + 1) + 8 * 2 * d) * N, 20.0 * N),
             300: ("cell build", (8.0 * d + 8 + 60 + 4 + 16 * (3 * d + 3)) * N, 0.0),
         }
@@ -379,7 +380,7 @@ class DemColumn(Workload):
         N = float(sc.n)
         self.n_active = sc.n
         self.kernels = {
-            108: ("dem_lsd contact sum", 88.0 * N, 8 * C),
+            108: ("dem_lsd contact sum", 88.0 * N, 0.0),
             301: ("symplectic integrator", 8.0 * 22 * N, 20.0 * N),
             300: ("cell build", (24.0 + 8 + 60 + 4 + 16 * 11) * N, 0.0),
         }
@@ -570,6 +571,7 @@ class DamBreakSlab(DamBreak):
         self.kernels = {
             200: ("density+EOS", (8.0 * d + 8 + 8) * N, 0.0),
             201: ("momentum G11+A", (8.0 * d * 3 + 16) * N, 0.0),
+            302: ("neighbour-list build", 20.0 * N, 0.0),
             301: ("symplectic integrator", (8.0 * (4 * d + 1) + 8 * 2 * d) * N, 20.0 * N),
             300: ("cell build", (8.0 * d + 8 + 60 + 4 + 16 * (3 * d + 5)) * N, 0.0),
         }

@@ -226,8 +226,7 @@ Geo make_geo(nau_ctx* c) {
     g.pre_abs = (float)(8.0 * ext_max * std::ldexp(1.0, -23));
     double cs_min = c->dom.cs[0];
     for (int a = 1; a < c->dom.dim; ++a) cs_min = std::fmin(cs_min, c->dom.cs[a]);
-    g.min_cs = (float)cs_min;
-    if ((double)g.min_cs > cs_min) g.min_cs = std::nextafter(g.min_cs, 0.0f);
+    g.min_cs = cs_min;
     for (int a = 0; a < 3; ++a) {
         g.img[a] = AxisImg{c->dom.ext[a], 2.0 * c->dom.lo[a], 2.0 * c->dom.hi[a], c->dom.cs[a]};
         g.lim[a] = a < c->dom.dim ? (float)(c->dom.cs[a] * 1.001) + g.pre_abs : 3.0e38f;

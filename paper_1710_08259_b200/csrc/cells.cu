@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_neighbor_counts(Geo g, const 
     double xi[3] = {0.0, 0.0, 0.0};
     for (int a = 0; a < DIM; ++a) xi[a] = g.x[a * g.n + kk];
     int cnt = 0;
-    sweep<DIM, false>(g, xl, k, valid, xi, (float)radius,
+    sweep<DIM, false>(g, xl, k, valid, xi, radius,
                [&](int, const double* rel, int) {
         if (norm_rel<DIM>(rel) <= radius) ++cnt;
     });
@@ -224,13 +224,14 @@ __global__ void __launch_bounds__(kSweepThreads) k_neighbor_counts(Geo g, const 
 // lane-interleaved list (sweep.cuh build_list). Per-lane loop, no warp votes.
 template <int DIM, bool ORDERED>
 __global__ void __launch_bounds__(kSweepThreads) k_nlist(const __grid_constant__ Geo g,
-                                                         const float4* xl, float pre_r,
+                                                         const float4* xl, double radius,
                                                          uint32_t* list, int* count, int cap,
                                                          int* over) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= *g.nact) return;
     uint32_t* lst = list + nlist_base(k, cap);
-    const int cnt = pre_r * 1.000001f <= g.min_cs
+    const float pre_r = (float)radius;
+    const int cnt = axis_mode(g, radius) < 2
                         ? build_list<DIM, ORDERED, false>(g, xl, k, pre_r, lst, cap)
                         : build_list<DIM, ORDERED, true>(g, xl, k, pre_r, lst, cap);
     count[k] = min(cnt, cap);
@@ -354,7 +355,7 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered) {
             c->nl_len = need;
         }
         cudaMemsetAsync(c->d_nover, 0, sizeof(int), c->stream);
-        const float r = (float)radius;
+        const double r = radius;
         prof_begin(c, 302);
         if (ordered) {
             switch (c->dom.dim) {

@@ -98,6 +98,10 @@ struct WcsphArgs {
     NList nl;
 };
 
+struct RhoPV {  // neighbour operands of the momentum pass
+    double rho, p, v[3];
+};
+
 // Pass 1: rho = sph_S(one, m, one, K, R) (interactions.cpp:40-58 with A = rho = 1),
 //         p = B*((rho/rho0)^gamma - 1).
 template <int DIM, int KF, bool LIST>
@@ -115,8 +119,8 @@ __global__ void __launch_bounds__(kThreads) k_wcsph_density(const __grid_constan
     const double alpha = kernel_alpha<KF>(a.kdim, h);
     const double s_unit = a.mass / 1.0;  // m_j / rho_j with the uniform operand rho = 1
     double acc = 0.0;
-    for_neighbors<DIM, true, LIST>(g, a.xl, a.nl, k, valid, xi, (float)radius,
-               [&](int, const double* rel, int) {
+    for_neighbors<DIM, true, LIST>(g, a.xl, a.nl, k, valid, xi, radius, NoLoad{},
+               [&](int, const double* rel, int, NoPayload) {
         const double dist = norm_rel<DIM>(rel);
         if (dist > radius) return;
         const double w = kernel_value<KF>(alpha, h, dist);
@@ -158,8 +162,17 @@ __global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_consta
     }
     const double pr_i = p_i / (rho_i * rho_i);
     double G[3] = {0.0, 0.0, 0.0}, A[3] = {0.0, 0.0, 0.0};
-    for_neighbors<DIM, true, LIST>(g, a.xl, a.nl, k, valid, xi, (float)radius,
-               [&](int j, const double* rel, int mask) {
+    // per-neighbour operands, gathered ahead of the pair arithmetic (consume_list)
+    auto load = [&](int j) {
+        RhoPV r;
+        r.rho = a.rho[j];
+        r.p = a.p[j];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) r.v[d] = d < DIM ? a.v[d * n + j] : 0.0;
+        return r;
+    };
+    for_neighbors<DIM, true, LIST>(g, a.xl, a.nl, k, valid, xi, radius, load,
+               [&](int j, const double* rel, int mask, const RhoPV& pj) {
         const double dist = norm_rel<DIM>(rel);
         if (dist > radius) return;
         if (dist <= 0.0) {  // G11 skips silently; sph_A warns (interactions.cpp:32-38)
@@ -167,18 +180,18 @@ __global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_consta
             return;
         }
         const double sc = kernel_grad_scale<KF>(alpha, h, dist);
-        const double rho_j = a.rho[j];
+        const double rho_j = pj.rho;
         if (rho_j == 0.0) {
             latch_error(a.err, 1, kMsgZeroDensity, g.orig[j]);
             return;
         }
-        const double s = m * (pr_i + a.p[j] / (rho_j * rho_j));
+        const double s = m * (pr_i + pj.p / (rho_j * rho_j));
 #pragma unroll
         for (int d = 0; d < DIM; ++d) G[d] = G[d] + (rel[d] * sc) * s;
-        double ap = (mirror_comp(a.v[j], 0, DIM, 1, mask, DIM) - v_i[0]) * rel[0];
+        double ap = (mirror_comp(pj.v[0], 0, DIM, 1, mask, DIM) - v_i[0]) * rel[0];
 #pragma unroll
         for (int d = 1; d < DIM; ++d)
-            ap = ap + (mirror_comp(a.v[d * n + j], d, DIM, 1, mask, DIM) - v_i[d]) * rel[d];
+            ap = ap + (mirror_comp(pj.v[d], d, DIM, 1, mask, DIM) - v_i[d]) * rel[d];
         if (ap >= 0.0) return;
         const double pi_ij = ap / (rho_i * dist * dist);
         const double sa = m * pi_ij;

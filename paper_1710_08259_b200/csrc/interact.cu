@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kThreads) k_sph(const __grid_constant__ SphArg
     for (int c = 0; c < 9; ++c) acc[c] = 0.0;
     const int my_orig = g.orig[kk];
 
-    sweep<DIM, true>(g, a.xl, k, valid, xi, (float)radius,
+    sweep<DIM, true>(g, a.xl, k, valid, xi, radius,
                [&](int j, const double* rel, int mask) {
         const double dist = norm_rel<DIM>(rel);
         if (OP == NAU_OP_SPH_S) {  // interactions.cpp:40-58
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kThreads) k_dem(const __grid_constant__ DemArg
     }
     const int my_orig = g.orig[kk];
     double acc[3] = {0.0, 0.0, 0.0};
-    sweep<DIM, true>(g, a.xl, k, valid, xi, (float)radius,
+    sweep<DIM, true>(g, a.xl, k, valid, xi, radius,
                [&](int j, const double* rel, int mask) {
         const double dist = norm_rel<DIM>(rel);
         if (dist > radius) return;

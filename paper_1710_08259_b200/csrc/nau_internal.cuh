@@ -74,7 +74,7 @@ struct Geo {
     const double4* p4;  // positions packed (x, y, z, 0) per slot, for gathers
     float lim[3];    // fp32 pre-filter per-axis limit: cell size * (1 + 1e-3) + pre_abs
     float pre_abs;   // absolute fp32 error bound of u = x - lo differences (8 ulp of extent)
-    float min_cs;    // smallest cell size, rounded down to fp32
+    double min_cs;   // smallest cell size
     long n;
     const double* x;  // pos component 0..dim-1 (x + a*n)
     const int* key;

@@ -93,10 +93,22 @@ __device__ __forceinline__ void option_of(const DomainDev& d, int a, int ci, con
     }
 }
 
+// Per-axis cell test (|rel_a| > cell size rejects, particle_system.hpp:120-126).
+// AX = 0: implied by the radius test for accepted pairs (radius < every cell
+//         size with an fp64 rounding margin), skipped;
+// AX = 1: exact fp64 test on the pre-filter survivors only (radius ~ cell size:
+//         the fp32 sphere pre-filter already bounds every axis);
+// AX = 2: also in the fp32 pre-filter (radius clearly above a cell size).
+// The pre-filter is a superset filter either way; only the fp64 test decides.
+__device__ __forceinline__ int axis_mode(const Geo& g, double radius) {
+    if (radius * (1.0 + 0x1p-40) < g.min_cs) return 0;
+    return radius <= 1.01 * g.min_cs ? 1 : 2;
+}
+
 // The sweep. Must be called by all 32 lanes of a warp (valid = false for lanes
 // without a particle). `pre_r` is the pre-filter radius (>= the operator's
 // acceptance radius).
-template <int DIM, bool ORDERED, bool AXIS, class Fn>
+template <int DIM, bool ORDERED, int AX, class Fn>
 __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restrict__ xl4, int k,
                                            bool valid, const double* xi, float pre_r,
                                            SweepSmem& sm, Fn& fn) {
@@ -163,22 +175,20 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
     };
     if (!done) advance();
 
-    // When the acceptance radius is <= every cell size, |rel_a| <= |rel| <= R makes
-    // the per-axis cell test redundant for accepted pairs (AXIS = false; chosen
-    // warp-uniformly by sweep() below).
-    constexpr bool axis_implied = !AXIS;
+    // per-axis tests: see axis_mode (AX chosen warp-uniformly by sweep() below)
+    constexpr bool axis_implied = AX == 0;
     auto test = [&](const float4 p) {
         const float r0 = fmaf(sg[0], p.x, bq[0]);
-        bool rej = !axis_implied && fabsf(r0) > g.lim[0];
+        bool rej = AX == 2 && fabsf(r0) > g.lim[0];
         float r2 = r0 * r0;
         if (DIM > 1) {
             const float r1 = fmaf(sg[1], p.y, bq[1]);
-            rej |= !axis_implied && fabsf(r1) > g.lim[1];
+            rej |= AX == 2 && fabsf(r1) > g.lim[1];
             r2 = fmaf(r1, r1, r2);
         }
         if (DIM > 2) {
             const float r3 = fmaf(sg[2], p.z, bq[2]);
-            rej |= !axis_implied && fabsf(r3) > g.lim[2];
+            rej |= AX == 2 && fabsf(r3) > g.lim[2];
             r2 = fmaf(r3, r3, r2);
         }
         return !(rej || r2 > r2lim);
@@ -281,6 +291,7 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
 // candidate order, into a lane-interleaved list: entry s of slot k lives at
 // list[((k/32)*cap + s)*32 + k%32] (coalesced for a warp). The passes then only
 // consume their list (consume_list). Same order as the sweep => same sums.
+// AXIS = the fp32 pre-filter's per-axis test (axis_mode == 2).
 template <int DIM, bool ORDERED, bool AXIS>
 __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict__ xl4, int k,
                                           float pre_r, uint32_t* lst, int cap) {
@@ -341,13 +352,48 @@ __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict
             return !(rej || r2 > r2lim);
         };
         int t = s;
+        for (; t + 8 <= e; t += 8) {  // eight loads in flight
+            float4 p[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) p[u] = xl4[t + u];
+            bool acc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[u] = test(p[u]);
+            const uint32_t v = (uint32_t)t | icode;
+            if (cnt + 8 <= cap) {
+                unsigned c = (unsigned)cnt;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (acc[u]) lst[c * 32u] = v + u;
+                    c += acc[u];
+                }
+                cnt = (int)c;
+            } else {
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (acc[u]) {
+                        if (cnt < cap) lst[cnt * 32] = v + u;
+                        ++cnt;
+                    }
+            }
+        }
         for (; t + 4 <= e; t += 4) {
             const float4 p0 = xl4[t], p1 = xl4[t + 1], p2 = xl4[t + 2], p3 = xl4[t + 3];
             const bool a0 = test(p0), a1 = test(p1), a2 = test(p2), a3 = test(p3);
-            if (a0) { if (cnt < cap) lst[cnt * 32] = (uint32_t)t | icode; ++cnt; }
-            if (a1) { if (cnt < cap) lst[cnt * 32] = (uint32_t)(t + 1) | icode; ++cnt; }
-            if (a2) { if (cnt < cap) lst[cnt * 32] = (uint32_t)(t + 2) | icode; ++cnt; }
-            if (a3) { if (cnt < cap) lst[cnt * 32] = (uint32_t)(t + 3) | icode; ++cnt; }
+            const uint32_t v = (uint32_t)t | icode;
+            if (cnt + 4 <= cap) {  // common case: predicated stores, no branches
+                const unsigned c0 = (unsigned)cnt, c1 = c0 + a0, c2 = c1 + a1, c3 = c2 + a2;
+                if (a0) lst[c0 * 32u] = v;
+                if (a1) lst[c1 * 32u] = v + 1;
+                if (a2) lst[c2 * 32u] = v + 2;
+                if (a3) lst[c3 * 32u] = v + 3;
+                cnt = (int)(c3 + a3);
+            } else {
+                if (a0) { if (cnt < cap) lst[cnt * 32] = v; ++cnt; }
+                if (a1) { if (cnt < cap) lst[cnt * 32] = v + 1; ++cnt; }
+                if (a2) { if (cnt < cap) lst[cnt * 32] = v + 2; ++cnt; }
+                if (a3) { if (cnt < cap) lst[cnt * 32] = v + 3; ++cnt; }
+            }
         }
         for (; t < e; ++t)
             if (test(xl4[t])) {
@@ -358,21 +404,34 @@ __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict
     return cnt;
 }
 
-// Evaluate fn over a slot's list (lane-private loop; the next gather is in flight
-// while the current pair is evaluated).
-template <int DIM, bool AXIS, class Fn>
+// Evaluate fn(j, rel, mask, payload) over a slot's list, payload = load(j) (the
+// pair's per-neighbour operands). Lane-private loop, software-pipelined: list
+// entries are fetched 4 pairs ahead and the position / payload gathers 2 pairs
+// ahead, so three dependent memory latencies overlap the pair arithmetic
+// (profiles/r1_nl_*: the one-ahead version stalled on long_scoreboard ~11 cycles
+// per issued instruction). AXIS = the exact fp64 per-axis test (axis_mode >= 1).
+template <int DIM, bool AXIS, class Load, class Fn>
 __device__ __forceinline__ void consume_list(const Geo& g, const uint32_t* __restrict__ lst, int cnt,
-                                             const double* xi, Fn&& fn) {
-    uint32_t ent_n = cnt > 0 ? lst[0] : 0u;
-    double4 pj_n = cnt > 0 ? g.p4[ent_n & ((1u << kSlotBits) - 1)] : make_double4(0, 0, 0, 0);
+                                             const double* xi, Load&& load, Fn&& fn) {
+    constexpr uint32_t kM = (1u << kSlotBits) - 1;
+    auto ent_at = [&](int s) { return s < cnt ? lst[s * 32] : 0u; };
+    uint32_t e0 = ent_at(0), e1 = ent_at(1), e2 = ent_at(2), e3 = ent_at(3);
+    double4 q0 = g.p4[e0 & kM], q1 = g.p4[e1 & kM];
+    auto l0 = load((int)(e0 & kM));
+    auto l1 = load((int)(e1 & kM));
     for (int s = 0; s < cnt; ++s) {
-        const uint32_t ent = ent_n;
-        const double4 pj = pj_n;
-        if (s + 1 < cnt) {
-            ent_n = lst[(s + 1) * 32];
-            pj_n = g.p4[ent_n & ((1u << kSlotBits) - 1)];
-        }
-        const int j = (int)(ent & ((1u << kSlotBits) - 1));
+        const uint32_t ent = e0;
+        const double4 pj = q0;
+        const auto pl = l0;
+        e0 = e1;
+        e1 = e2;
+        e2 = e3;
+        e3 = ent_at(s + 4);
+        q0 = q1;
+        l0 = l1;
+        q1 = g.p4[e1 & kM];  // pair s + 2
+        l1 = load((int)(e1 & kM));
+        const int j = (int)(ent & kM);
         const int c = (int)(ent >> kSlotBits);
         const double xj[3] = {pj.x, pj.y, pj.z};
         double rel[3] = {0.0, 0.0, 0.0};
@@ -394,23 +453,31 @@ __device__ __forceinline__ void consume_list(const Geo& g, const uint32_t* __res
                 mask |= (cc[a] >= 3) << a;
             }
         }
-        if (ok) fn(j, rel, mask);
+        if (ok) fn(j, rel, mask, pl);
     }
 }
 
-// Entry point: picks the per-axis-test-free instantiation when every lane's
-// pre-filter radius is below the smallest cell size (min_cs is rounded down; the
-// 1e-6 factor covers the rounding of pre_r), which is the case for every
-// BASELINE deck (radius = cell size / 1.0 or less).
+struct NoPayload {};
+struct NoLoad {
+    __device__ __forceinline__ NoPayload operator()(int) const { return NoPayload{}; }
+};
+
+// Entry point: `radius` is the lane's acceptance radius (fp64); the per-axis
+// mode is the warp's maximum of axis_mode (BASELINE decks: radius = cell size,
+// mode 1).
 template <int DIM, bool ORDERED, class Fn>
 __device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ xl4, int k,
-                                      bool valid, const double* xi, float pre_r, Fn&& fn) {
+                                      bool valid, const double* xi, double radius, Fn&& fn) {
     __shared__ SweepSmem smem[kSweepThreads / 32];
     SweepSmem& sm = smem[threadIdx.x >> 5];
-    if (__all_sync(0xffffffffu, !valid || pre_r * 1.000001f <= g.min_cs))
-        sweep_impl<DIM, ORDERED, false>(g, xl4, k, valid, xi, pre_r, sm, fn);
+    const float pre_r = (float)radius;
+    const int ax = __reduce_max_sync(0xffffffffu, valid ? axis_mode(g, radius) : 0);
+    if (ax == 0)
+        sweep_impl<DIM, ORDERED, 0>(g, xl4, k, valid, xi, pre_r, sm, fn);
+    else if (ax == 1)
+        sweep_impl<DIM, ORDERED, 1>(g, xl4, k, valid, xi, pre_r, sm, fn);
     else
-        sweep_impl<DIM, ORDERED, true>(g, xl4, k, valid, xi, pre_r, sm, fn);
+        sweep_impl<DIM, ORDERED, 2>(g, xl4, k, valid, xi, pre_r, sm, fn);
 }
 
 struct NList {  // per-step neighbour lists (k_nlist in cells.cu)
@@ -423,22 +490,24 @@ __device__ __forceinline__ size_t nlist_base(int k, int cap) {
     return (size_t)(k >> 5) * cap * 32 + (k & 31);
 }
 
-// fn over k's neighbour candidates: from the step's list (LIST) or a fresh sweep.
-// Both visit the same candidates in the same order.
-template <int DIM, bool ORDERED, bool LIST, class Fn>
+// fn(j, rel, mask, load(j)) over k's neighbour candidates: from the step's list
+// (LIST) or a fresh sweep. Both visit the same candidates in the same order.
+template <int DIM, bool ORDERED, bool LIST, class Load, class Fn>
 __device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __restrict__ xl4,
                                               const NList& nl, int k, bool valid,
-                                              const double* xi, float pre_r, Fn&& fn) {
+                                              const double* xi, double radius, Load&& load,
+                                              Fn&& fn) {
     if constexpr (LIST) {
         if (!valid) return;
         const uint32_t* lst = nl.e + nlist_base(k, nl.cap);
         const int cnt = nl.count[k];
-        if (pre_r * 1.000001f <= g.min_cs)
-            consume_list<DIM, false>(g, lst, cnt, xi, fn);
+        if (axis_mode(g, radius) == 0)
+            consume_list<DIM, false>(g, lst, cnt, xi, load, fn);
         else
-            consume_list<DIM, true>(g, lst, cnt, xi, fn);
+            consume_list<DIM, true>(g, lst, cnt, xi, load, fn);
     } else {
-        sweep<DIM, ORDERED>(g, xl4, k, valid, xi, pre_r, fn);
+        sweep<DIM, ORDERED>(g, xl4, k, valid, xi, radius,
+                            [&](int j, const double* rel, int mask) { fn(j, rel, mask, load(j)); });
     }
 }
 
