@@ -292,6 +292,21 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
 // list[((k/32)*cap + s)*32 + k%32] (coalesced for a warp). The passes then only
 // consume their list (consume_list). Same order as the sweep => same sums.
 // AXIS = the fp32 pre-filter's per-axis test (axis_mode == 2).
+//
+// Predicated list store: address = lane base + c * 128 B in one wide multiply-add
+// (the compiler otherwise rebuilds the 64-bit address from the kernel parameter
+// for every candidate, ~10 instructions per store).
+__device__ __forceinline__ void st_list_if(uint32_t* base, unsigned c, uint32_t v, bool p) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t.reg .u64 a;\n\t"
+        "setp.ne.u32 q, %3, 0;\n\t"
+        "mad.wide.u32 a, %1, 128, %0;\n\t"
+        "@q st.global.u32 [a], %2;\n\t}"
+        :
+        : "l"(base), "r"(c), "r"(v), "r"((unsigned)p)
+        : "memory");
+}
+
 template <int DIM, bool ORDERED, bool AXIS>
 __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict__ xl4, int k,
                                           float pre_r, uint32_t* lst, int cap) {
@@ -351,55 +366,49 @@ __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict
             }
             return !(rej || r2 > r2lim);
         };
-        int t = s;
-        for (; t + 8 <= e; t += 8) {  // eight loads in flight
-            float4 p[8];
+        // Blocks of 32 candidates: the tests set a bit mask (eight loads in flight,
+        // tail loads clamped and masked off), then the set bits are expanded
+        // into list entries - ~1/6 of the candidates, instead of a predicated
+        // store sequence for every candidate.
+        for (int t = s; t < e; t += 32) {
+            const int nb = min(32, e - t);
+            uint32_t m = 0;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) p[u] = xl4[t + u];
-            bool acc[8];
+            for (int u0 = 0; u0 < 32; u0 += 8) {
+                if (u0 + 8 <= nb) {
+                    const float4* q = xl4 + t + u0;
+                    float4 p[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc[u] = test(p[u]);
+                    for (int u = 0; u < 8; ++u) p[u] = q[u];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) m |= (uint32_t)test(p[u]) << (u0 + u);
+                } else if (u0 < nb) {  // tail: clamped loads, masked below
+                    float4 p[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) p[u] = xl4[min(t + u0 + u, e - 1)];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) m |= (uint32_t)test(p[u]) << (u0 + u);
+                }
+            }
+            if (nb < 32) m &= (1u << nb) - 1u;
             const uint32_t v = (uint32_t)t | icode;
-            if (cnt + 8 <= cap) {
+            if (cnt + __popc(m) <= cap) {
                 unsigned c = (unsigned)cnt;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (acc[u]) lst[c * 32u] = v + u;
-                    c += acc[u];
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    st_list_if(lst, c++, v + b, true);
                 }
                 cnt = (int)c;
             } else {
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (acc[u]) {
-                        if (cnt < cap) lst[cnt * 32] = v + u;
-                        ++cnt;
-                    }
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    if (cnt < cap) lst[cnt * 32] = v + b;
+                    ++cnt;
+                }
             }
         }
-        for (; t + 4 <= e; t += 4) {
-            const float4 p0 = xl4[t], p1 = xl4[t + 1], p2 = xl4[t + 2], p3 = xl4[t + 3];
-            const bool a0 = test(p0), a1 = test(p1), a2 = test(p2), a3 = test(p3);
-            const uint32_t v = (uint32_t)t | icode;
-            if (cnt + 4 <= cap) {  // common case: predicated stores, no branches
-                const unsigned c0 = (unsigned)cnt, c1 = c0 + a0, c2 = c1 + a1, c3 = c2 + a2;
-                if (a0) lst[c0 * 32u] = v;
-                if (a1) lst[c1 * 32u] = v + 1;
-                if (a2) lst[c2 * 32u] = v + 2;
-                if (a3) lst[c3 * 32u] = v + 3;
-                cnt = (int)(c3 + a3);
-            } else {
-                if (a0) { if (cnt < cap) lst[cnt * 32] = v; ++cnt; }
-                if (a1) { if (cnt < cap) lst[cnt * 32] = v + 1; ++cnt; }
-                if (a2) { if (cnt < cap) lst[cnt * 32] = v + 2; ++cnt; }
-                if (a3) { if (cnt < cap) lst[cnt * 32] = v + 3; ++cnt; }
-            }
-        }
-        for (; t < e; ++t)
-            if (test(xl4[t])) {
-                if (cnt < cap) lst[cnt * 32] = (uint32_t)t | icode;
-                ++cnt;
-            }
     }
     return cnt;
 }
