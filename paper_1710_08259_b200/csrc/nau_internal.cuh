@@ -93,6 +93,17 @@ struct FieldBuf {
     int comps() const { return rows * cols; }
 };
 
+// 32-byte gather in ONE load instruction (sm_100: LDG.E.ENL2.256). The pair
+// gathers of the neighbour sums are bound by L1 wavefronts; a double4 read as
+// two 128-bit loads costs two (profiles/r1_nl_*: L1/TEX throughput ~85%).
+__device__ __forceinline__ double4 ld256(const double4* p) {
+    double4 v;
+    asm("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+        : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+        : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ void latch_error(DevErr* e, int code, int msg, long long particle) {
     atomicOr(&e->code, code);
     if (code & 1) {

@@ -208,13 +208,13 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
         // the current pair is evaluated (profiles/r1_v5: the gather's latency was the
         // top stall of the drain)
         uint32_t ent_n = took > 0 ? qe[(head & (kQueue - 1)) * 32] : 0u;
-        double4 pj_n = took > 0 ? g.p4[ent_n & ((1u << kSlotBits) - 1)] : make_double4(0, 0, 0, 0);
+        double4 pj_n = took > 0 ? ld256(g.p4 + (ent_n & ((1u << kSlotBits) - 1))) : make_double4(0, 0, 0, 0);
         for (int s = 0; s < steps; ++s) {
             const uint32_t ent = ent_n;
             const double4 pj = pj_n;  // one 32-byte sector per pair
             if (s + 1 < took) {
                 ent_n = qe[((head + s + 1) & (kQueue - 1)) * 32];
-                pj_n = g.p4[ent_n & ((1u << kSlotBits) - 1)];
+                pj_n = ld256(g.p4 + (ent_n & ((1u << kSlotBits) - 1)));
             }
             if (s < fill) {
                 const int j = (int)(ent & ((1u << kSlotBits) - 1));
@@ -425,7 +425,7 @@ __device__ __forceinline__ void consume_list(const Geo& g, const uint32_t* __res
     constexpr uint32_t kM = (1u << kSlotBits) - 1;
     auto ent_at = [&](int s) { return s < cnt ? lst[s * 32] : 0u; };
     uint32_t e0 = ent_at(0), e1 = ent_at(1), e2 = ent_at(2), e3 = ent_at(3);
-    double4 q0 = g.p4[e0 & kM], q1 = g.p4[e1 & kM];
+    double4 q0 = ld256(g.p4 + (e0 & kM)), q1 = ld256(g.p4 + (e1 & kM));
     auto l0 = load((int)(e0 & kM));
     auto l1 = load((int)(e1 & kM));
     for (int s = 0; s < cnt; ++s) {
@@ -438,7 +438,7 @@ __device__ __forceinline__ void consume_list(const Geo& g, const uint32_t* __res
         e3 = ent_at(s + 4);
         q0 = q1;
         l0 = l1;
-        q1 = g.p4[e1 & kM];  // pair s + 2
+        q1 = ld256(g.p4 + (e1 & kM));  // pair s + 2
         l1 = load((int)(e1 & kM));
         const int j = (int)(ent & kM);
         const int c = (int)(ent >> kSlotBits);
