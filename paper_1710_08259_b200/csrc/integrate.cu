@@ -96,10 +96,7 @@ struct WcsphArgs {
     double* vdot;
     DevErr* err;
     NList nl;
-};
-
-struct RhoPV {  // neighbour operands of the momentum pass
-    double rho, p, v[3];
+    double4* vp;  // (vx, vy, vz, p / (rho * rho)) per slot, written by the density pass
 };
 
 // Pass 1: rho = sph_S(one, m, one, K, R) (interactions.cpp:40-58 with A = rho = 1),
@@ -132,6 +129,12 @@ __global__ void __launch_bounds__(kThreads) k_wcsph_density(const __grid_constan
     if (!isfinite(acc) || !isfinite(p)) latch_error(a.err, 2, kMsgNan, g.orig[k]);
     a.rho[k] = acc;
     a.p[k] = p;
+    // the momentum pass's per-neighbour operands in one 32-byte record; p/(rho*rho)
+    // is the reference's per-pair subexpression (interactions.cpp:97), same value
+    double vv[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) vv[d] = a.v[d * n + k];
+    a.vp[k] = make_double4(vv[0], vv[1], vv[2], p / (acc * acc));
 }
 
 // Pass 2: vdot = -1/rho*sph_G11(p,m,rho,K,R) + visc*sph_A(v,m,rho,K,R) + g, one
@@ -162,17 +165,10 @@ __global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_consta
     }
     const double pr_i = p_i / (rho_i * rho_i);
     double G[3] = {0.0, 0.0, 0.0}, A[3] = {0.0, 0.0, 0.0};
-    // per-neighbour operands, gathered ahead of the pair arithmetic (consume_list)
-    auto load = [&](int j) {
-        RhoPV r;
-        r.rho = a.rho[j];
-        r.p = a.p[j];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) r.v[d] = d < DIM ? a.v[d * n + j] : 0.0;
-        return r;
-    };
-    for_neighbors<DIM, true, LIST>(g, a.xl, a.nl, k, valid, xi, radius, load,
-               [&](int j, const double* rel, int mask, const RhoPV& pj) {
+    // per-neighbour operands (v_j, p_j / rho_j^2), gathered ahead of the pair arithmetic
+    auto load = [&](int j) { return ld256(a.vp + j); };
+    for_neighbors<DIM, true, LIST, false, 2>(g, a.xl, a.nl, k, valid, xi, radius, load,
+               [&](int j, const double* rel, int mask, const double4& pj) {
         const double dist = norm_rel<DIM>(rel);
         if (dist > radius) return;
         if (dist <= 0.0) {  // G11 skips silently; sph_A warns (interactions.cpp:32-38)
@@ -180,18 +176,19 @@ __global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_consta
             return;
         }
         const double sc = kernel_grad_scale<KF>(alpha, h, dist);
-        const double rho_j = pj.rho;
-        if (rho_j == 0.0) {
+        const double pr_j = pj.w;  // non-finite only if rho_j == 0 or p_j overflowed
+        if (!isfinite(pr_j) && a.rho[j] == 0.0) {
             latch_error(a.err, 1, kMsgZeroDensity, g.orig[j]);
             return;
         }
-        const double s = m * (pr_i + pj.p / (rho_j * rho_j));
+        const double s = m * (pr_i + pr_j);
 #pragma unroll
         for (int d = 0; d < DIM; ++d) G[d] = G[d] + (rel[d] * sc) * s;
-        double ap = (mirror_comp(pj.v[0], 0, DIM, 1, mask, DIM) - v_i[0]) * rel[0];
+        const double vj[3] = {pj.x, pj.y, pj.z};
+        double ap = (mirror_comp(vj[0], 0, DIM, 1, mask, DIM) - v_i[0]) * rel[0];
 #pragma unroll
         for (int d = 1; d < DIM; ++d)
-            ap = ap + (mirror_comp(pj.v[d], d, DIM, 1, mask, DIM) - v_i[d]) * rel[d];
+            ap = ap + (mirror_comp(vj[d], d, DIM, 1, mask, DIM) - v_i[d]) * rel[d];
         if (ap >= 0.0) return;
         const double pi_ij = ap / (rho_i * dist * dist);
         const double sa = m * pi_ij;
@@ -306,6 +303,7 @@ void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p, bool lists) {
     if (c->n == 0) return;
     WcsphArgs a;
     a.nl = NList{lists ? c->d_nlist : nullptr, c->d_ncount, c->nl_cap};
+    a.vp = c->d_aux;
     a.g = make_geo(c);
     a.xl = c->d_xl;
     a.mass = p->mass;

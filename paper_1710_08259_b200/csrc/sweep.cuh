@@ -414,42 +414,40 @@ __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict
 }
 
 // Evaluate fn(j, rel, mask, payload) over a slot's list, payload = load(j) (the
-// pair's per-neighbour operands). Lane-private loop, software-pipelined: list
-// entries are fetched 4 pairs ahead and the position / payload gathers 2 pairs
-// ahead, so three dependent memory latencies overlap the pair arithmetic
-// (profiles/r1_nl_*: the one-ahead version stalled on long_scoreboard ~11 cycles
-// per issued instruction). AXIS = the exact fp64 per-axis test (axis_mode >= 1).
-template <int DIM, bool AXIS, class Load, class Fn>
+// pair's per-neighbour operands). Lane-private loop, software-pipelined: the
+// position / payload gathers run 2 pairs ahead of the arithmetic and the list
+// entries 4-5 pairs ahead, in three buffers with fixed roles (loop unrolled by
+// 3: no register rotation; profiles/r1_nl_*: the rotating version spent ~30
+// moves per pair and the one-ahead version stalled on long_scoreboard).
+// AXIS = the exact fp64 per-axis test. FAST drops the reference's "+ 0.0" of the
+// direct image (it only normalises -0.0; FAST mode does not promise bitwise).
+template <int DIM, bool AXIS, bool FAST, int NB, class Load, class Fn>
 __device__ __forceinline__ void consume_list(const Geo& g, const uint32_t* __restrict__ lst, int cnt,
                                              const double* xi, Load&& load, Fn&& fn) {
     constexpr uint32_t kM = (1u << kSlotBits) - 1;
+    using P = decltype(load(0));
+    struct Buf {
+        uint32_t ent;
+        double4 p;
+        P pl;
+    };
     auto ent_at = [&](int s) { return s < cnt ? lst[s * 32] : 0u; };
-    uint32_t e0 = ent_at(0), e1 = ent_at(1), e2 = ent_at(2), e3 = ent_at(3);
-    double4 q0 = ld256(g.p4 + (e0 & kM)), q1 = ld256(g.p4 + (e1 & kM));
-    auto l0 = load((int)(e0 & kM));
-    auto l1 = load((int)(e1 & kM));
-    for (int s = 0; s < cnt; ++s) {
-        const uint32_t ent = e0;
-        const double4 pj = q0;
-        const auto pl = l0;
-        e0 = e1;
-        e1 = e2;
-        e2 = e3;
-        e3 = ent_at(s + 4);
-        q0 = q1;
-        l0 = l1;
-        q1 = ld256(g.p4 + (e1 & kM));  // pair s + 2
-        l1 = load((int)(e1 & kM));
-        const int j = (int)(ent & kM);
-        const int c = (int)(ent >> kSlotBits);
-        const double xj[3] = {pj.x, pj.y, pj.z};
+    auto fetch = [&](Buf& b, uint32_t ent) {
+        b.ent = ent;
+        b.p = ld256(g.p4 + (ent & kM));
+        b.pl = load((int)(ent & kM));
+    };
+    auto process = [&](const Buf& b) {
+        const int j = (int)(b.ent & kM);
+        const int c = (int)(b.ent >> kSlotBits);
+        const double xj[3] = {b.p.x, b.p.y, b.p.z};
         double rel[3] = {0.0, 0.0, 0.0};
         bool ok = true;
         int mask = 0;
         if (c == 0) {
 #pragma unroll
             for (int a = 0; a < DIM; ++a) {
-                rel[a] = (xj[a] + 0.0) - xi[a];
+                rel[a] = FAST ? xj[a] - xi[a] : (xj[a] + 0.0) - xi[a];
                 ok &= !AXIS || !(fabs(rel[a]) > g.img[a].cs);
             }
         } else {
@@ -462,7 +460,36 @@ __device__ __forceinline__ void consume_list(const Geo& g, const uint32_t* __res
                 mask |= (cc[a] >= 3) << a;
             }
         }
-        if (ok) fn(j, rel, mask, pl);
+        if (ok) fn(j, rel, mask, b.pl);
+    };
+    if constexpr (NB == 3) {
+        Buf A, B, C;
+        uint32_t eA = ent_at(3), eB = ent_at(4), eC = ent_at(2);
+        fetch(A, ent_at(0));
+        fetch(B, ent_at(1));
+        for (int s = 0; s < cnt; s += 3) {
+            fetch(C, eC);  // pair s + 2
+            eC = ent_at(s + 5);
+            process(A);  // pair s
+            fetch(A, eA);  // pair s + 3
+            eA = ent_at(s + 6);
+            if (s + 1 < cnt) process(B);
+            fetch(B, eB);  // pair s + 4
+            eB = ent_at(s + 7);
+            if (s + 2 < cnt) process(C);
+        }
+    } else {  // two buffers: gathers one pair ahead (register-lean)
+        Buf A, B;
+        uint32_t eA = ent_at(2), eB = ent_at(1);
+        fetch(A, ent_at(0));
+        for (int s = 0; s < cnt; s += 2) {
+            fetch(B, eB);  // pair s + 1
+            eB = ent_at(s + 3);
+            process(A);  // pair s
+            fetch(A, eA);  // pair s + 2
+            eA = ent_at(s + 4);
+            if (s + 1 < cnt) process(B);
+        }
     }
 }
 
@@ -501,7 +528,11 @@ __device__ __forceinline__ size_t nlist_base(int k, int cap) {
 
 // fn(j, rel, mask, load(j)) over k's neighbour candidates: from the step's list
 // (LIST) or a fresh sweep. Both visit the same candidates in the same order.
-template <int DIM, bool ORDERED, bool LIST, class Load, class Fn>
+// FAST (the FAST-mode kernels, whose smoothing kernels vanish at the support
+// radius): the per-axis test is skipped whenever radius <= every cell size —
+// a pair it would reject has |rel| > cell size >= radius up to one rounding,
+// i.e. q = 2 where W and dW/dq are zero.
+template <int DIM, bool ORDERED, bool LIST, bool FAST = false, int NB = 3, class Load, class Fn>
 __device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __restrict__ xl4,
                                               const NList& nl, int k, bool valid,
                                               const double* xi, double radius, Load&& load,
@@ -510,10 +541,11 @@ __device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __rest
         if (!valid) return;
         const uint32_t* lst = nl.e + nlist_base(k, nl.cap);
         const int cnt = nl.count[k];
-        if (axis_mode(g, radius) == 0)
-            consume_list<DIM, false>(g, lst, cnt, xi, load, fn);
+        const bool axis = FAST ? !(radius <= g.min_cs) : axis_mode(g, radius) != 0;
+        if (!axis)
+            consume_list<DIM, false, FAST, NB>(g, lst, cnt, xi, load, fn);
         else
-            consume_list<DIM, true>(g, lst, cnt, xi, load, fn);
+            consume_list<DIM, true, FAST, NB>(g, lst, cnt, xi, load, fn);
     } else {
         sweep<DIM, ORDERED>(g, xl4, k, valid, xi, radius,
                             [&](int j, const double* rel, int mask) { fn(j, rel, mask, load(j)); });
