@@ -335,6 +335,10 @@ void nau_destroy(nau_ctx* c) {
     dfree(c->d_nlist);
     dfree(c->d_ncount);
     dfree(c->d_nover);
+    dfree(c->d_hq);
+    dfree(c->d_pstart);
+    dfree(c->d_pcount);
+    dfree(c->d_hesc);
     if (c->h_err) cudaFreeHost(c->h_err);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

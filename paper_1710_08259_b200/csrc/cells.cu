@@ -9,6 +9,9 @@
 //                    (cells_[c] holds ascending i, particle_system.cpp:37-51)
 //     5. k_reorder   one gather pass permuting every SoA field + orig/key/active
 // All passes are streaming (HBM-bound); see DESIGN.md for the per-particle bytes.
+#include <cstdio>
+#include <cstdlib>
+
 #include "nau_internal.cuh"
 #include "sweep.cuh"
 
@@ -226,16 +229,53 @@ template <int DIM, bool ORDERED>
 __global__ void __launch_bounds__(kSweepThreads) k_nlist(const __grid_constant__ Geo g,
                                                          const float4* xl, double radius,
                                                          uint32_t* list, int* count, int cap,
-                                                         int* over) {
+                                                         int* over, const __grid_constant__ HalfGrid hg) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= *g.nact) return;
     uint32_t* lst = list + nlist_base(k, cap);
     const float pre_r = (float)radius;
-    const int cnt = axis_mode(g, radius) < 2
-                        ? build_list<DIM, ORDERED, false>(g, xl, k, pre_r, lst, cap)
-                        : build_list<DIM, ORDERED, true>(g, xl, k, pre_r, lst, cap);
+    int cnt;
+    if (hg.on && *hg.escaped == 0)
+        cnt = build_list_half<DIM, ORDERED>(g, hg, k, lst, cap);
+    else
+        cnt = axis_mode(g, radius) < 2 ? build_list<DIM, ORDERED, false>(g, xl, k, pre_r, lst, cap)
+                                       : build_list<DIM, ORDERED, true>(g, xl, k, pre_r, lst, cap);
     count[k] = min(cnt, cap);
     if (cnt > cap) atomicMax(over, cnt);
+}
+
+// fp16 cell-relative coordinates (sweep.cuh HalfGrid): padded cell sizes, then one
+// scatter per slot; the last slot of each cell writes its cell's +inf pads.
+__global__ void k_pcount(int nc, const int* count, int* pcount) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c <= nc) pcount[c] = c < nc ? (count[c] + 7) & ~7 : 0;
+}
+
+__global__ void k_half_coords(DomainDev d, long n, const double* pos, const int* key,
+                              const int* cell_start, const int* cell_count, const int* pstart,
+                              long hlen, __half* h, int* escaped) {
+    const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int c = key[k];
+    if (c >= d.ncells) return;  // inactive tail
+    const long rank = k - cell_start[c];
+    const long p = pstart[c] + rank;
+    int rem = c;
+    bool esc = false;
+    for (int a = 0; a < d.dim; ++a) {
+        const int ca = rem % d.cells[a];
+        rem /= d.cells[a];
+        const double q = (pos[a * n + k] - d.lo[a]) / d.cs[a] - (double)ca;
+        esc |= !(q >= -1e-3 && q <= 1.001);
+        h[a * hlen + p] = __double2half(q);  // round to nearest
+    }
+    if (esc) atomicOr(escaped, 1);
+    if (rank == cell_count[c] - 1) {
+        const __half inf = __ushort_as_half((unsigned short)0x7c00);
+        const long pe = pstart[c] + ((cell_count[c] + 7) & ~7);
+        for (long q = p + 1; q < pe; ++q)
+            for (int a = 0; a < d.dim; ++a) h[a * hlen + q] = inf;
+    }
 }
 
 __global__ void k_unsort(long n, int comps, const int* orig, const double* src, double* dst) {
@@ -325,6 +365,61 @@ void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig) {
     c->launches++;
 }
 
+// fp16 pre-filter data for the list build (sweep.cuh HalfGrid), rebuilt once per
+// cell build. Off (fp32 pre-filter) for anisotropic cells or radius > 1.5 cells.
+static HalfGrid half_grid(nau_ctx* c, double radius) {
+    HalfGrid hg{};
+    const DomainDev& d = c->dom;
+    const int nc = d.ncells;
+    bool iso = true;
+    for (int a = 1; a < d.dim; ++a) iso &= d.cs[a] == d.cs[0];
+    const double rho = radius / d.cs[0];
+    if (!iso || !(rho <= 1.5) || c->n == 0) return hg;
+    // padded cells plus 32 halves of slack (build_list_half reads whole 32-blocks)
+    const long hlen = ((c->n + 8L * (nc + 1) + 32) + 7) & ~7L;
+    if (c->hq_len < hlen) {
+        if (c->d_hq) cudaFree(c->d_hq);
+        c->d_hq = nullptr;
+        c->hq_len = 0;
+        if (cudaMalloc(&c->d_hq, sizeof(__half) * 3 * hlen) != cudaSuccess) {
+            cudaGetLastError();
+            return hg;
+        }
+        c->hq_len = hlen;
+        c->hq_rev = -1;
+    }
+    if (c->pstart_len < nc + 1) {
+        if (c->d_pstart) cudaFree(c->d_pstart);
+        if (c->d_pcount) cudaFree(c->d_pcount);
+        c->d_pstart = c->d_pcount = nullptr;
+        c->pstart_len = 0;
+        if (cudaMalloc(&c->d_pstart, sizeof(int) * (nc + 1)) != cudaSuccess ||
+            cudaMalloc(&c->d_pcount, sizeof(int) * (nc + 1)) != cudaSuccess) {
+            cudaGetLastError();
+            return hg;
+        }
+        c->pstart_len = nc + 1;
+        c->hq_rev = -1;
+    }
+    if (!c->d_hesc && cudaMalloc(&c->d_hesc, sizeof(int)) != cudaSuccess) return hg;
+    if (c->hq_rev != c->rebuild_count) {
+        k_pcount<<<blocks_for(nc + 1), kBlock, 0, c->stream>>>(nc, c->d_cell_count, c->d_pcount);
+        scan_exclusive(c, c->d_pcount, c->d_pstart, nc + 1);
+        cudaMemsetAsync(c->d_hesc, 0, sizeof(int), c->stream);
+        k_half_coords<<<blocks_for(c->n), kBlock, 0, c->stream>>>(
+            d, c->n, c->fields[0].d, c->d_key, c->d_cell_start, c->d_cell_count, c->d_pstart,
+            c->hq_len, c->d_hq, c->d_hesc);
+        c->launches += 2;
+        c->hq_rev = c->rebuild_count;
+    }
+    for (int a = 0; a < 3; ++a) hg.h[a] = c->d_hq + a * c->hq_len;
+    hg.pstart = c->d_pstart;
+    hg.escaped = c->d_hesc;
+    hg.rho = (float)rho;
+    hg.on = 1;
+    return hg;
+}
+
 bool build_nlist(nau_ctx* c, double radius, bool ordered) {
     const long n = c->n;
     if (n == 0 || !c->use_nlist) return false;
@@ -342,6 +437,7 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered) {
     Geo g = make_geo(c);
     const int T = kSweepThreads;
     const int b = blocks_for(n, T);
+    const HalfGrid hg = half_grid(c, radius);
     for (int attempt = 0; attempt < 3; ++attempt) {
         const size_t need = slots * (size_t)c->nl_cap;
         if (c->nl_len < need) {
@@ -359,15 +455,15 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered) {
         prof_begin(c, 302);
         if (ordered) {
             switch (c->dom.dim) {
-                case 1: k_nlist<1, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
-                case 2: k_nlist<2, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
-                default: k_nlist<3, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
+                case 1: k_nlist<1, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
+                case 2: k_nlist<2, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
+                default: k_nlist<3, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
             }
         } else {
             switch (c->dom.dim) {
-                case 1: k_nlist<1, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
-                case 2: k_nlist<2, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
-                default: k_nlist<3, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover); break;
+                case 1: k_nlist<1, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
+                case 2: k_nlist<2, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
+                default: k_nlist<3, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
             }
         }
         prof_end(c, 302);

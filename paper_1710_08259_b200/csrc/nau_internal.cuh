@@ -12,6 +12,7 @@
 // neighbour-sum kernels read each cell's particles as a contiguous range.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -351,6 +352,15 @@ struct nau_ctx {
     long nc_len = 0;
     int* d_nover = nullptr;  // max list length seen when > cap (0 = fits)
     int nl_cap = 0;
+    // fp16 cell-relative coordinates in a cell-padded layout (sweep.cuh HalfGrid),
+    // rebuilt lazily after each cell build
+    __half* d_hq = nullptr;  // 3 x hq_len
+    long hq_len = 0;
+    int* d_pstart = nullptr;  // ncells + 1
+    int* d_pcount = nullptr;  // ncells + 1 (rounded-up counts, scan input)
+    long pstart_len = 0;
+    int* d_hesc = nullptr;    // escape flag
+    long hq_rev = -1;         // rebuild_count the fp16 copy belongs to
     int mode = NAU_MODE_EXACT;
     int* d_cell_start = nullptr;  // ncells + 2
     int* d_cell_count = nullptr;  // ncells + 1

@@ -516,6 +516,159 @@ __device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ x
         sweep_impl<DIM, ORDERED, 2>(g, xl4, k, valid, xi, pre_r, sm, fn);
 }
 
+// ---- half-precision pre-filter for the list build ------------------------------
+// Isotropic cells, radius <= 1.5 cell sizes, every particle inside its cell's
+// box (else the fp32 build_list runs). Each particle's coordinates relative to
+// its cell origin, in cell units, are stored as fp16 in a cell-padded layout
+// (every cell's range starts at a multiple of 8, pads = +inf), so one 128-bit
+// load brings 8 candidates per axis and HFMA2 tests two candidates per
+// instruction: rel_a = sg * h_j + (off_a - h_i), off_a = the option's cell offset
+// (-1, 0, 1; mirror-low 0 with sg = -1; mirror-high 2 with sg = -1).
+// Error bound (cell units): |h| < 1 rounds to 2^-12, off - h_i (|.| <= 2) to
+// 2^-11, the HFMA2 result (|rel| <= 2 near the threshold) to 2^-11: |rel error|
+// <= 1.25 * 2^-10; |rel| <= rho => sqrt(r2) <= rho + 0.0022 before the three
+// r2 roundings (<= 2^-10 each for r2 < 4): r2 <= (rho + 0.0022)^2 + 0.003 =: lim,
+// rounded up to fp16. A superset filter again; the fp64 test decides.
+struct HalfGrid {
+    const __half* h[3];  // padded per-axis coordinates
+    const int* pstart;   // padded start of each cell (multiple of 8)
+    const int* escaped;  // set by the build when some particle lies outside its cell box
+    float rho;           // radius / cell size
+    int on;              // host-side eligibility (isotropic, rho <= 1.5)
+};
+
+__device__ __forceinline__ float half_offset(const AxisOpts& ao, int ci, int o, float& sg,
+                                             int& icode, int& cell, int n, int kind) {
+    if (o < ao.ndir) {
+        const int off = ao.lo_off + o;
+        int c = ci + off;
+        icode = 0;
+        if (c < 0) {
+            c += n;
+            icode = 2;
+        } else if (c >= n) {
+            c -= n;
+            icode = 1;
+        }
+        cell = c;
+        sg = 1.0f;
+        return (float)off;
+    }
+    sg = -1.0f;
+    if (o == ao.ndir && ci == 0) {
+        cell = 0;
+        icode = 3;
+        return 0.0f;
+    }
+    cell = n - 1;
+    icode = 4;
+    return 2.0f;
+}
+
+template <int DIM, bool ORDERED>
+__device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg, int k,
+                                               uint32_t* lst, int cap) {
+    const DomainDev& d = g.dom;
+    const int flat_i = g.key[k];
+    int ci[3] = {0, 0, 0};
+    decode_cell<DIM>(d, flat_i, ci);
+    AxisOpts ao[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ao[a] = AxisOpts{0, 1, 1};
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) ao[a] = axis_opts(d, a, ci[a]);
+    const int pk = hg.pstart[flat_i] + (k - g.cell_start[flat_i]);
+    float hi[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) hi[a] = __half2float(hg.h[a][pk]);
+    const float rl = hg.rho + 0.0022f;
+    const __half2 lim2 = __half2half2(__float2half_ru(fmaf(rl, rl, 0.003f)));
+    const int n01 = ao[0].cnt * (DIM > 1 ? ao[1].cnt : 1);
+    const int ncombo = n01 * (DIM > 2 ? ao[2].cnt : 1);
+    // option setup; the next option's cell-table reads are issued one option
+    // ahead (a lane's 27 options are otherwise a chain of dependent latencies)
+    struct Opt {
+        __half2 sg2[3], bq2[3];
+        uint32_t icode;
+        int s, ns, ps;
+    };
+    auto setup = [&](int idx, Opt& o) {
+        const int combo = ORDERED ? idx : ((idx & 1) ? ncombo - 1 - (idx >> 1) : (idx >> 1));
+        const int oo[3] = {combo % ao[0].cnt, DIM > 1 ? (combo / ao[0].cnt) % ao[1].cnt : 0,
+                           DIM > 2 ? combo / n01 : 0};
+        int flat = 0, code = 0, stride = 1, scode = 1;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            float sg;
+            int ic, cell;
+            const float off = half_offset(ao[a], ci[a], oo[a], sg, ic, cell, d.cells[a], d.kind[a]);
+            o.sg2[a] = __float2half2_rn(sg);
+            o.bq2[a] = __float2half2_rn(off - hi[a]);
+            flat += stride * cell;
+            code += scode * ic;
+            stride *= d.cells[a];
+            scode *= 5;
+        }
+        o.icode = (uint32_t)code << kSlotBits;
+        o.s = g.cell_start[flat];
+        o.ns = g.cell_count[flat];
+        o.ps = hg.pstart[flat];
+    };
+    int cnt = 0;
+    Opt nxt;
+    setup(0, nxt);
+    for (int idx = 0; idx < ncombo; ++idx) {
+        const Opt o = nxt;
+        if (idx + 1 < ncombo) setup(idx + 1, nxt);
+        for (int q0 = 0; q0 < o.ns; q0 += 32) {
+            // all four 8-candidate groups loaded up front (the padded layout has
+            // slack past the last cell; lanes past the cell are masked below)
+            uint4 hv[4][3];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int a = 0; a < DIM; ++a)
+                    hv[u][a] = *reinterpret_cast<const uint4*>(hg.h[a] + o.ps + q0 + 8 * u);
+            uint32_t m = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t* w[3] = {&hv[u][0].x, &hv[u][1].x, &hv[u][2].x};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    __half2 r2;
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) {
+                        const __half2 x2 = *reinterpret_cast<const __half2*>(w[a] + q);
+                        const __half2 r = __hfma2(o.sg2[a], x2, o.bq2[a]);
+                        r2 = a == 0 ? __hmul2(r, r) : __hfma2(r, r, r2);
+                    }
+                    const unsigned mk = __hle2_mask(r2, lim2);
+                    m |= ((mk & 1u) | ((mk >> 15) & 2u)) << (8 * u + 2 * q);
+                }
+            }
+            if (o.ns - q0 < 32) m &= (1u << (o.ns - q0)) - 1u;
+            const uint32_t v = (uint32_t)(o.s + q0) | o.icode;
+            if (cnt + __popc(m) <= cap) {
+                unsigned c = (unsigned)cnt;
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    st_list_if(lst, c++, v + b, true);
+                }
+                cnt = (int)c;
+            } else {
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    if (cnt < cap) lst[cnt * 32] = v + b;
+                    ++cnt;
+                }
+            }
+        }
+    }
+    return cnt;
+}
+
 struct NList {  // per-step neighbour lists (k_nlist in cells.cu)
     const uint32_t* e;
     const int* count;

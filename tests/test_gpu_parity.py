@@ -352,13 +352,17 @@ def _run_deck(build, fast, lists, steps):
         c.close()
 
 
-def _random_deck(n, seed, kind, radius):
+def _random_deck(n, seed, kind, radius, outside=0):
     """n random particles in the unit square, 4 x 4 cells of 0.25 (lists of up
-    to ~n pi radius^2 entries: exercises the list capacity growth/fallback)."""
+    to ~n pi radius^2 entries: exercises the list capacity growth/fallback).
+    `outside` particles are moved just past x = 1 (clamped into the last cell
+    column of a symmetric axis: the fp16 list pre-filter must step aside)."""
     def build(c):
         rng = np.random.default_rng(seed)
         c.set_domain(2, [0, 0], [4, 4], [0.25, 0.25], [kind, kind])
-        c.set_particles(rng.random((2, n)))
+        pos = rng.random((2, n))
+        pos[0, :outside] = 1.0 + 0.02 * rng.random(outside)
+        c.set_particles(pos)
         c.add_field("rho", 1, 1, 0.0)
         c.add_field("p", 1, 1, 0.0)
         c.add_field("v", 2, 1, 0.01 * rng.standard_normal((2, n)))
@@ -388,13 +392,17 @@ def test_neighbor_lists_identical_to_sweep_dam3d(fast):
         np.testing.assert_array_equal(on[k], off[k], err_msg=k)
 
 
-@pytest.mark.parametrize("n,radius,kind", [(8000, 0.25, nau.PERIODIC),
-                                           (8000, 0.25, nau.SYMMETRIC),
-                                           (24000, 0.25, nau.PERIODIC)])
-def test_neighbor_lists_capacity_growth_and_fallback(n, radius, kind):
+@pytest.mark.parametrize("n,radius,kind,outside", [(8000, 0.25, nau.PERIODIC, 0),
+                                                   (8000, 0.25, nau.SYMMETRIC, 0),
+                                                   (24000, 0.25, nau.PERIODIC, 0),
+                                                   (3000, 0.45, nau.SYMMETRIC, 0),
+                                                   (3000, 0.25, nau.SYMMETRIC, 7)])
+def test_neighbor_lists_capacity_growth_and_fallback(n, radius, kind, outside):
     """~1600 entries per list (capacity grows from 64 in one retry) and ~4700 (above
-    the list cap: the step falls back to sweeping) give the sweep's results."""
-    build = _random_deck(n, 77, kind, radius)
+    the list cap: the step falls back to sweeping) give the sweep's results; so do
+    the fp32 list pre-filter (radius 1.8 cells) and particles outside their cell
+    box (fp16 pre-filter disabled at run time)."""
+    build = _random_deck(n, 77, kind, radius, outside)
     for fast in (False, True):
         on, _ = _run_deck(build, fast, True, 2)
         off, _ = _run_deck(build, fast, False, 2)
