@@ -262,11 +262,11 @@ class Microbench(Workload):
         ctx.interact("sph_L0", ["A", prm["mass"], "rho", prm["radius"]], "L", kernel=self.kw)
 
     def e2e_step(self, ctx):
-        ctx.upload_ptr("r", self.h_pos.data_ptr())
-        ctx.upload_ptr("A", self.h_A.data_ptr())
+        ctx.upload_async("r", self.h_pos.data_ptr())
+        ctx.upload_async("A", self.h_A.data_ptr())
         self.step(ctx)
         for f, t in zip(("rho", "G", "L"), self.h_out):
-            ctx.download_ptr(f, t.data_ptr())
+            ctx.download_async(f, t.data_ptr())
 
     def config(self):
         return {"workload": self.name, "particles": self.sc.n, "cells": "44^3 periodic",
@@ -335,11 +335,11 @@ class DamBreak(Workload):
         ctx.wcsph_step(self.p)
 
     def e2e_step(self, ctx):
-        ctx.upload_ptr("r", self.h_r.data_ptr())
-        ctx.upload_ptr("v", self.h_v.data_ptr())
+        ctx.upload_async("r", self.h_r.data_ptr())
+        ctx.upload_async("v", self.h_v.data_ptr())
         self.step(ctx)
         for k, t in self.h_out.items():
-            ctx.download_ptr(k, t.data_ptr())
+            ctx.download_async(k, t.data_ptr())
 
     def config(self):
         sc = self.sc
@@ -396,11 +396,11 @@ class DemColumn(Workload):
         ctx.dem_step(self.p)
 
     def e2e_step(self, ctx):
-        ctx.upload_ptr("r", self.h_r.data_ptr())
-        ctx.upload_ptr("v", self.h_v.data_ptr())
+        ctx.upload_async("r", self.h_r.data_ptr())
+        ctx.upload_async("v", self.h_v.data_ptr())
         self.step(ctx)
         for k, t in self.h_out.items():
-            ctx.download_ptr(k, t.data_ptr())
+            ctx.download_async(k, t.data_ptr())
 
     def config(self):
         sc = self.sc
@@ -443,11 +443,11 @@ class Gravity(Workload):
         ctx.leapfrog_step(self.p)
 
     def e2e_step(self, ctx):
-        ctx.upload_ptr("r", self.h_r.data_ptr())
-        ctx.upload_ptr("v", self.h_v.data_ptr())
+        ctx.upload_async("r", self.h_r.data_ptr())
+        ctx.upload_async("v", self.h_v.data_ptr())
         self.step(ctx)
         for k, t in self.h_out.items():
-            ctx.download_ptr(k, t.data_ptr())
+            ctx.download_async(k, t.data_ptr())
 
     def config(self):
         return {"workload": self.name, "particles": self.sc.n, "pairs_per_step": self.sc.n ** 2}
@@ -696,6 +696,27 @@ def timed_steps(ctx, fn, steps, flush):
     return sum(a.elapsed_time(b) for a, b in evs)
 
 
+def timed_pipelined(ctx, fn, steps):
+    """K end-to-end steps as ONE device-timed interval: the context's copy streams are
+    fenced after the start event and joined before the stop event, so every step's
+    H2D and D2H copy lies inside it while copies overlap neighbouring steps' passes.
+    No L2 flush: each step streams > 126 MB (L2) of host data in and out."""
+    import torch
+    stream = torch.cuda.ExternalStream(ctx.L.nau_get_stream(ctx.h))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        ctx.io_fence()
+        for _ in range(steps):
+            fn(ctx)
+        ctx.io_join()
+        e1.record(stream)
+    stream.synchronize()
+    ctx.sync()
+    return e0.elapsed_time(e1)
+
+
 def run_ours(args, dist):
     import torch
     from paper_1710_08259_b200 import nau
@@ -732,7 +753,7 @@ def run_ours(args, dist):
     for _ in range(2):
         wl.e2e_step(ctx)
     dist.barrier()
-    ms_e2e = dist.max(timed_steps(ctx, wl.e2e_step, args.steps, flush))
+    ms_e2e = dist.max(timed_pipelined(ctx, wl.e2e_step, args.steps))
     e2e = n_total * args.steps / (ms_e2e * 1e-3)
     # ---- roofline of the dominant kernel ----
     peaks, peak_kind = measured_peaks()
@@ -779,7 +800,12 @@ def run_ours(args, dist):
                        l2="flushed between timed steps (256 MiB memset, untimed)"),
         "e2e": {"value": round(e2e, 1), "unit": "particle-updates/s",
                 "h2d_bytes_per_step": int(wl.h2d), "d2h_bytes_per_step": int(wl.d2h),
-                "ms_per_step": round(ms_e2e / args.steps, 4)},
+                "ms_per_step": round(ms_e2e / args.steps, 4),
+                "timing": ("K steps as one device interval; per step r, v (A) uploaded from "
+                           "and results downloaded to pinned host memory via "
+                           "nau_upload_async / nau_download_async (copy streams overlap "
+                           "neighbouring steps' passes); no L2 flush: each step streams "
+                           "more than L2 through host copies")},
         "gpu_launches": int(launches),
         "roofline": roofline,
         "kernels": per_kernel,

@@ -125,6 +125,18 @@ nau_status nau_free_field(nau_ctx* ctx, int field_id);
 /* host SoA, component-major [c*n + i] with c = col*rows + row, original order */
 nau_status nau_upload(nau_ctx* ctx, int field_id, const double* soa, long n);
 nau_status nau_download(nau_ctx* ctx, int field_id, double* soa, long n);
+/* Asynchronous host I/O (same layout as nau_upload / nau_download). The copies run
+ * on the context's copy streams (one per direction) through per-field
+ * double-buffered staging, so a step's uploads and downloads overlap the
+ * neighbour passes of the steps around it. Host buffers should be pinned; an
+ * upload's source must stay unchanged, and a download's destination is valid,
+ * only after nau_sync. nau_io_fence orders later copies after the work enqueued
+ * so far on the context stream; nau_io_join makes the context stream wait for
+ * every enqueued copy (a device-side join, e.g. before a timing event). */
+nau_status nau_upload_async(nau_ctx* ctx, int field_id, const double* soa, long n);
+nau_status nau_download_async(nau_ctx* ctx, int field_id, double* soa, long n);
+nau_status nau_io_fence(nau_ctx* ctx);
+nau_status nau_io_join(nau_ctx* ctx);
 /* Uniform value (rows*cols doubles, column-major) into every particle. */
 nau_status nau_fill(nau_ctx* ctx, int field_id, const double* value);
 nau_status nau_copy_field(nau_ctx* ctx, int dst, int src);

@@ -187,6 +187,10 @@ void reset_err(nau_ctx* c) {
 
 // Fetch and clear the device error word; map it to a status.
 nau_status collect(nau_ctx* c) {
+    if (c->s_h2d) {  // asynchronous host I/O completes here too
+        cudaStreamSynchronize(c->s_h2d);
+        cudaStreamSynchronize(c->s_d2h);
+    }
     cudaError_t ce = cudaStreamSynchronize(c->stream);
     if (ce != cudaSuccess) return fail(c, NAU_ERR_CUDA, cudaGetErrorString(ce));
     ce = cudaGetLastError();
@@ -323,10 +327,17 @@ nau_status nau_create(int device, nau_ctx** out) {
     return NAU_OK;
 }
 
+static void io_release(nau_ctx* c);
+
 void nau_destroy(nau_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    if (c->s_h2d) {
+        cudaStreamSynchronize(c->s_h2d);
+        cudaStreamSynchronize(c->s_d2h);
+    }
     if (c->stream) cudaStreamSynchronize(c->stream);
+    io_release(c);
     free_particles(c);
     free_cells(c);
     dfree(c->d_err);
@@ -414,6 +425,10 @@ nau_status nau_set_particles(nau_ctx* c, long n, const double* pos_soa) {
         return fail(c, NAU_ERR_ARG,
                     "particle count must be below 2^25 per context (shard larger systems across GPUs)");
     cudaSetDevice(c->device);
+    if (c->s_h2d) {
+        cudaStreamSynchronize(c->s_h2d);
+        cudaStreamSynchronize(c->s_d2h);
+    }
     cudaStreamSynchronize(c->stream);
     free_particles(c);
     c->n = n;
@@ -517,6 +532,114 @@ nau_status nau_download(nau_ctx* c, int id, double* soa, long n) {
     NAU_CUDA(cudaMemcpyAsync(soa, f.alt, sizeof(double) * n * f.comps(), cudaMemcpyDeviceToHost,
                              c->stream));
     return collect(c);
+}
+
+// ---- asynchronous host I/O -----------------------------------------------------
+// Uploads: H2D into staging buffer b on s_h2d, then the context stream scatters it
+// into cell order (k_sort_in). Downloads: the context stream gathers into staging
+// buffer b (k_unsort), then D2H on s_d2h. Two buffers per field and direction, each
+// guarded by events, so step k's copies overlap step k+-1's passes.
+static nau_status io_prepare(nau_ctx* c, std::vector<nau_ctx::IoStage>& v, int id, size_t len) {
+    if (!c->s_h2d) {
+        NAU_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+        NAU_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    }
+    if ((int)v.size() <= id) v.resize(id + 1);
+    nau_ctx::IoStage& st = v[id];
+    if (st.len < len) {
+        cudaStreamSynchronize(c->s_h2d);
+        cudaStreamSynchronize(c->s_d2h);
+        cudaStreamSynchronize(c->stream);
+        for (int b = 0; b < 2; ++b) {
+            dfree(st.buf[b]);
+            NAU_CUDA(dalloc(&st.buf[b], len));
+            if (!st.ready[b]) NAU_CUDA(cudaEventCreateWithFlags(&st.ready[b], cudaEventDisableTiming));
+            if (!st.consumed[b])
+                NAU_CUDA(cudaEventCreateWithFlags(&st.consumed[b], cudaEventDisableTiming));
+        }
+        st.len = len;
+    }
+    return NAU_OK;
+}
+
+static void io_release(nau_ctx* c) {
+    for (auto* v : {&c->io_up, &c->io_down})
+        for (auto& st : *v)
+            for (int b = 0; b < 2; ++b) {
+                dfree(st.buf[b]);
+                if (st.ready[b]) cudaEventDestroy(st.ready[b]);
+                if (st.consumed[b]) cudaEventDestroy(st.consumed[b]);
+            }
+    c->io_up.clear();
+    c->io_down.clear();
+    if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+    c->s_h2d = c->s_d2h = nullptr;
+}
+
+nau_status nau_upload_async(nau_ctx* c, int id, const double* soa, long n) {
+    if (!field_ok(c, id) || n != c->n) return fail(c, NAU_ERR_ARG, "bad field id or count");
+    if (n == 0) return NAU_OK;
+    FieldBuf& f = c->fields[id];
+    const size_t len = (size_t)n * f.comps();
+    nau_status s = io_prepare(c, c->io_up, id, len);
+    if (s != NAU_OK) return s;
+    nau_ctx::IoStage& st = c->io_up[id];
+    const int b = st.next;
+    st.next ^= 1;
+    NAU_CUDA(cudaStreamWaitEvent(c->s_h2d, st.consumed[b], 0));  // previous scatter read it
+    NAU_CUDA(cudaMemcpyAsync(st.buf[b], soa, sizeof(double) * len, cudaMemcpyHostToDevice, c->s_h2d));
+    NAU_CUDA(cudaEventRecord(st.ready[b], c->s_h2d));
+    NAU_CUDA(cudaStreamWaitEvent(c->stream, st.ready[b], 0));
+    nau::launch_sort_in(c, st.buf[b], f.d, f.comps());
+    NAU_CUDA(cudaEventRecord(st.consumed[b], c->stream));
+    if (id == 0) c->dirty = true;
+    return NAU_OK;
+}
+
+nau_status nau_download_async(nau_ctx* c, int id, double* soa, long n) {
+    if (!field_ok(c, id) || n != c->n) return fail(c, NAU_ERR_ARG, "bad field id or count");
+    if (n == 0) return NAU_OK;
+    FieldBuf& f = c->fields[id];
+    const size_t len = (size_t)n * f.comps();
+    nau_status s = io_prepare(c, c->io_down, id, len);
+    if (s != NAU_OK) return s;
+    nau_ctx::IoStage& st = c->io_down[id];
+    const int b = st.next;
+    st.next ^= 1;
+    NAU_CUDA(cudaStreamWaitEvent(c->stream, st.consumed[b], 0));  // previous D2H read it
+    nau::launch_unsort(c, f.d, st.buf[b], f.comps());
+    NAU_CUDA(cudaEventRecord(st.ready[b], c->stream));
+    NAU_CUDA(cudaStreamWaitEvent(c->s_d2h, st.ready[b], 0));
+    NAU_CUDA(cudaMemcpyAsync(soa, st.buf[b], sizeof(double) * len, cudaMemcpyDeviceToHost, c->s_d2h));
+    NAU_CUDA(cudaEventRecord(st.consumed[b], c->s_d2h));
+    return NAU_OK;
+}
+
+nau_status nau_io_fence(nau_ctx* c) {
+    if (!c->s_h2d) {
+        NAU_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+        NAU_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    }
+    cudaEvent_t e;
+    NAU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEventRecord(e, c->stream);
+    cudaStreamWaitEvent(c->s_h2d, e, 0);
+    cudaStreamWaitEvent(c->s_d2h, e, 0);
+    cudaEventDestroy(e);  // released once the waits are satisfied
+    return NAU_OK;
+}
+
+nau_status nau_io_join(nau_ctx* c) {
+    if (!c->s_h2d) return NAU_OK;
+    for (cudaStream_t s : {c->s_h2d, c->s_d2h}) {
+        cudaEvent_t e;
+        NAU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        cudaEventRecord(e, s);
+        cudaStreamWaitEvent(c->stream, e, 0);
+        cudaEventDestroy(e);
+    }
+    return NAU_OK;
 }
 
 nau_status nau_fill(nau_ctx* c, int id, const double* value) {

@@ -361,6 +361,17 @@ struct nau_ctx {
     long pstart_len = 0;
     int* d_hesc = nullptr;    // escape flag
     long hq_rev = -1;         // rebuild_count the fp16 copy belongs to
+    // asynchronous host I/O (nau_upload_async / nau_download_async): one copy
+    // stream per direction, per-field double-buffered staging in original order
+    struct IoStage {
+        double* buf[2] = {nullptr, nullptr};
+        size_t len = 0;                        // doubles per buffer
+        cudaEvent_t ready[2] = {nullptr, nullptr};     // data in buf[b] is complete
+        cudaEvent_t consumed[2] = {nullptr, nullptr};  // buf[b] may be overwritten
+        int next = 0;
+    };
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    std::vector<IoStage> io_up, io_down;  // indexed by field id
     int mode = NAU_MODE_EXACT;
     int* d_cell_start = nullptr;  // ncells + 2
     int* d_cell_count = nullptr;  // ncells + 1

@@ -39,6 +39,7 @@ EXPORTS = [
     "nau_profile_ms", "nau_launch_count", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
     "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows", "nau_dem_step",
     "nau_leapfrog_step", "nau_pack_sources", "nau_gravity_sources", "nau_set_neighbor_lists",
+    "nau_upload_async", "nau_download_async", "nau_io_fence", "nau_io_join",
 ]
 
 
@@ -142,6 +143,10 @@ def load():
         "nau_pack_sources": (i, [vp, i, d, vp]),
         "nau_gravity_sources": (i, [vp, vp, l, l, d, d, i]),
         "nau_set_neighbor_lists": (i, [vp, i]),
+        "nau_upload_async": (i, [vp, i, vp, l]),
+        "nau_download_async": (i, [vp, i, vp, l]),
+        "nau_io_fence": (i, [vp]),
+        "nau_io_join": (i, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -294,6 +299,20 @@ class Context:
 
     def download_ptr(self, f, host_ptr):
         self._check(self.L.nau_download(self.h, self._fid(f), C.c_void_p(host_ptr), self.n))
+
+    def upload_async(self, f, host_ptr):
+        """Asynchronous upload from a pinned host buffer (complete at sync())."""
+        self._check(self.L.nau_upload_async(self.h, self._fid(f), C.c_void_p(host_ptr), self.n))
+
+    def download_async(self, f, host_ptr):
+        """Asynchronous download into a pinned host buffer (valid after sync())."""
+        self._check(self.L.nau_download_async(self.h, self._fid(f), C.c_void_p(host_ptr), self.n))
+
+    def io_fence(self):
+        self._check(self.L.nau_io_fence(self.h))
+
+    def io_join(self):
+        self._check(self.L.nau_io_join(self.h))
 
     def fill(self, f, value):
         v = np.zeros(9)

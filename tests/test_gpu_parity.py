@@ -410,6 +410,44 @@ def test_neighbor_lists_capacity_growth_and_fallback(n, radius, kind, outside):
             np.testing.assert_array_equal(on[k], off[k], err_msg=(fast, k))
 
 
+def test_async_host_io_matches_sync():
+    """nau_upload_async / nau_download_async (double-buffered staging on copy
+    streams) give the same per-step results as the synchronous calls."""
+    import torch
+    sc = scenes.dam_break(2)
+    outs = {}
+    for mode in ("sync", "async"):
+        c = nau.Context(0)
+        try:
+            p = _gpu_dam(c, sc)
+            h_r = torch.from_numpy(np.ascontiguousarray(sc.pos)).pin_memory()
+            h_v = torch.from_numpy(0.01 * np.ones((2, sc.n))).pin_memory()
+            res = []
+            for s in range(4):
+                bufs = {k: torch.empty((r, sc.n), dtype=torch.float64).pin_memory()
+                        for k, r in (("r", 2), ("v", 2), ("rho", 1))}
+                if mode == "sync":
+                    c.upload_ptr("r", h_r.data_ptr())
+                    c.upload_ptr("v", h_v.data_ptr())
+                    c.wcsph_step(p)
+                    for k, t in bufs.items():
+                        c.download_ptr(k, t.data_ptr())
+                else:
+                    c.upload_async("r", h_r.data_ptr())
+                    c.upload_async("v", h_v.data_ptr())
+                    c.wcsph_step(p)
+                    for k, t in bufs.items():
+                        c.download_async(k, t.data_ptr())
+                res.append(bufs)
+            c.sync()
+            outs[mode] = [{k: t.numpy().copy() for k, t in b.items()} for b in res]
+        finally:
+            c.close()
+    for a, b in zip(outs["sync"], outs["async"]):
+        for k in a:
+            np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
 # ------------------------------------------------------- slab primitives ----
 def test_select_pack_load_roundtrip(ctx):
     import torch
