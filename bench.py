@@ -243,6 +243,7 @@ class Microbench(Workload):
             100: ("sph_S density", 32.0 * N, 14 * nn),
             102: ("sph_G11 gradient", 64.0 * N, 24 * nn),
             103: ("sph_L0 Laplacian", 48.0 * N, 27 * nn),
+            302: ("neighbour-list build", 20.0 * N + 4.0 * nn, 0.0),
             300: ("cell build", (32.0 + 60.0 + 4.0 + 16.0 * 8) * N, 0.0),
         }
         self.cand_per_particle = C / N

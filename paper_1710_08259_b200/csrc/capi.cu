@@ -453,6 +453,8 @@ nau_status nau_set_particles(nau_ctx* c, long n, const double* pos_soa) {
     c->dirty = true;
     c->built_once = false;
     c->rebuild_count = 0;
+    c->nl_rev = -1;  // neighbour-list and fp16 caches belong to the old particle set
+    c->hq_rev = -1;
     c->warnings = 0;
     return collect(c);
 }
@@ -799,10 +801,17 @@ nau_status nau_interact(nau_ctx* c, int op, int kf, int kdim, const nau_operand*
                                  cudaMemcpyDeviceToDevice, c->stream));
         out = of.alt;
     }
-    if (c->mode == NAU_MODE_FAST && nau::fast_supports(op, ar, acl, dim))
-        nau::launch_interact_fast(c, op, kf, kdim, d_ops, out, ar);
+    const bool fast = c->mode == NAU_MODE_FAST && nau::fast_supports(op, ar, acl, dim);
+    // SPH operators with a uniform radius share the cell build's neighbour list
+    // (several operators per step walk the same candidates; same order either way)
+    bool lists = false;
+    if (op <= NAU_OP_SPH_A && ops[3].field_id < 0 && ops[3].value[0] > 0.0)
+        lists = nau::nlist_for(c, ops[3].value[0], !fast);
+    if (fast)
+        nau::launch_interact_fast(c, op, kf, kdim, d_ops, out, ar, lists);
     else
-        nau::launch_interact(c, op, kf, kdim, d_ops, nops, out, out_rows, out_cols, ar, acl);
+        nau::launch_interact(c, op, kf, kdim, d_ops, nops, out, out_rows, out_cols, ar, acl,
+                             nullptr, nullptr, lists);
     if (alias) std::swap(of.d, of.alt);
     return NAU_OK;
 }
@@ -844,7 +853,7 @@ nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
         if (s != NAU_OK) return s;
     }
     // Both passes of the step share one neighbour list (same candidates, same order).
-    const bool lists = nau::build_nlist(c, p->radius, c->mode == NAU_MODE_EXACT);
+    const bool lists = nau::nlist_for(c, p->radius, c->mode == NAU_MODE_EXACT);
     if (c->mode == NAU_MODE_FAST) {
         nau::launch_wcsph_fast(c, p, c->d_aux, lists);
         nau::launch_symplectic(c, c->fields[p->f_v].d, c->fields[p->f_vdot].d,

@@ -478,6 +478,18 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered) {
     return false;
 }
 
+bool nlist_for(nau_ctx* c, double radius, bool ordered) {
+    if (!c->use_nlist || c->n == 0) return false;
+    if (c->nl_rev == c->rebuild_count && c->nl_radius == radius && c->nl_ordered == ordered)
+        return true;
+    c->nl_rev = -1;
+    if (!build_nlist(c, radius, ordered)) return false;
+    c->nl_rev = c->rebuild_count;
+    c->nl_radius = radius;
+    c->nl_ordered = ordered;
+    return true;
+}
+
 void launch_unsort(nau_ctx* c, const double* d_src, double* d_dst, int comps) {
     if (c->n == 0) return;
     k_unsort<<<blocks_for(c->n), kBlock, 0, c->stream>>>(c->n, comps, c->d_orig, d_src, d_dst);

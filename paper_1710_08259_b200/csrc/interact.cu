@@ -29,9 +29,10 @@ struct SphArgs {
     int arows, acols;
     int kdim;
     DevErr* err;
+    NList nl;  // the cell build's neighbour list (uniform radius), or e == nullptr
 };
 
-template <int DIM, int OP, int KF, int AC>
+template <int DIM, int OP, int KF, int AC, bool LIST>
 __global__ void __launch_bounds__(kThreads) k_sph(const __grid_constant__ SphArgs a) {
     const Geo& g = a.g;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -68,8 +69,8 @@ __global__ void __launch_bounds__(kThreads) k_sph(const __grid_constant__ SphArg
     for (int c = 0; c < 9; ++c) acc[c] = 0.0;
     const int my_orig = g.orig[kk];
 
-    sweep<DIM, true>(g, a.xl, k, valid, xi, radius,
-               [&](int j, const double* rel, int mask) {
+    for_neighbors<DIM, true, LIST>(g, a.xl, a.nl, k, valid, xi, radius, NoLoad{},
+               [&](int j, const double* rel, int mask, NoPayload) {
         const double dist = norm_rel<DIM>(rel);
         if (OP == NAU_OP_SPH_S) {  // interactions.cpp:40-58
             if (dist > radius) return;
@@ -404,9 +405,11 @@ template <int DIM, int OP, int KF>
 void sph_launch(nau_ctx* c, const SphArgs& a, int ac) {
     const int blocks = (int)((c->n + kThreads - 1) / kThreads);
     if (OP == NAU_OP_SPH_S && ac > 1)
-        k_sph<DIM, OP, KF, 9><<<blocks, kThreads, 0, c->stream>>>(a);
+        k_sph<DIM, OP, KF, 9, false><<<blocks, kThreads, 0, c->stream>>>(a);
+    else if (a.nl.e)
+        k_sph<DIM, OP, KF, 1, true><<<blocks, kThreads, 0, c->stream>>>(a);
     else
-        k_sph<DIM, OP, KF, 1><<<blocks, kThreads, 0, c->stream>>>(a);
+        k_sph<DIM, OP, KF, 1, false><<<blocks, kThreads, 0, c->stream>>>(a);
 }
 
 template <int DIM, int OP>
@@ -443,7 +446,7 @@ void dem_dispatch(nau_ctx* c, int op, const DemArgs& a) {
 
 void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int nops, double* out,
                      int out_rows, int out_cols, int a_rows, int a_cols, const double* gadd,
-                     const GravSources* gsrc) {
+                     const GravSources* gsrc, bool lists) {
     (void)out_rows;
     (void)out_cols;
     if (c->n == 0) return;
@@ -461,6 +464,7 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
         a.acols = a_cols;
         a.kdim = kdim;
         a.err = c->d_err;
+        a.nl = NList{lists ? c->d_nlist : nullptr, c->d_ncount, c->nl_cap};
         const int ac = a_rows * a_cols;
         prof_begin(c, 100 + op);
         if (dim == 1) sph_dispatch<1>(c, op, a, kf, ac);

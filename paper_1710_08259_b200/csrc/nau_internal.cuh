@@ -352,6 +352,9 @@ struct nau_ctx {
     long nc_len = 0;
     int* d_nover = nullptr;  // max list length seen when > cap (0 = fits)
     int nl_cap = 0;
+    long nl_rev = -1;        // list cache key: cell build, radius, option order
+    double nl_radius = 0.0;
+    bool nl_ordered = false;
     // fp16 cell-relative coordinates in a cell-padded layout (sweep.cuh HalfGrid),
     // rebuilt lazily after each cell build
     __half* d_hq = nullptr;  // 3 x hq_len
@@ -408,6 +411,9 @@ void launch_boundary_shift(nau_ctx* c);
 void launch_build_cells(nau_ctx* c);
 void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig);
 bool build_nlist(nau_ctx* c, double radius, bool ordered);  // false: lists unusable this step
+// The current cell build's list for (radius, order), built on first use and shared
+// by every neighbour pass until the cells are rebuilt.
+bool nlist_for(nau_ctx* c, double radius, bool ordered);
 void launch_unsort(nau_ctx* c, const double* d_src, double* d_dst, int comps);
 void launch_sort_in(nau_ctx* c, const double* d_src_orig, double* d_dst, int comps);
 // interact.cu
@@ -417,7 +423,8 @@ struct GravSources {  // all-gathered (x, y, z, m) rows for sharded n-body
 };
 void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int nops,
                      double* out, int out_rows, int out_cols, int a_rows, int a_cols,
-                     const double* gadd = nullptr, const GravSources* gsrc = nullptr);
+                     const double* gadd = nullptr, const GravSources* gsrc = nullptr,
+                     bool lists = false);
 // integrate.cu
 void launch_euler(nau_ctx* c, const double* x, const double* xdot, double dt, double* out,
                   int comps);
@@ -427,6 +434,6 @@ void launch_reduce(nau_ctx* c, int kind, const double* f, int comps, double* h_o
 // fast.cu
 bool fast_supports(int op, int a_rows, int a_cols, int dim);
 void launch_interact_fast(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, double* out,
-                          int a_rows);
+                          int a_rows, bool lists = false);
 void launch_wcsph_fast(nau_ctx* c, const nau_wcsph_params* p, double4* vp, bool lists);
 }  // namespace nau
