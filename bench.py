@@ -240,9 +240,9 @@ class Microbench(Workload):
         N = float(sc.n)
         # per-particle bytes / flops
         self.kernels = {
-            100: ("sph_S density", 32.0 * N, 14 * nn),
-            102: ("sph_G11 gradient", 64.0 * N, 24 * nn),
-            103: ("sph_L0 Laplacian", 48.0 * N, 27 * nn),
+            100: ("sph_S density", 32.0 * N + 4.0 * nn, 14 * nn),
+            102: ("sph_G11 gradient", 64.0 * N + 4.0 * nn, 24 * nn),
+            103: ("sph_L0 Laplacian", 48.0 * N + 4.0 * nn, 27 * nn),
             302: ("neighbour-list build", 20.0 * N + 4.0 * nn, 0.0),
             300: ("cell build", (32.0 + 60.0 + 4.0 + 16.0 * 8) * N, 0.0),
         }
@@ -316,8 +316,9 @@ class DamBreak(Workload):
         d = sc.dim
         self.n_active = sc.n
         self.kernels = {
-            200: ("density+EOS", (8.0 * d + 8 + 8) * N, 14 * nn + 10 * N),
-            201: ("momentum G11+A", (8.0 * d * 3 + 16) * N, 42 * nn),
+            # + 4 B per list entry (>= one per neighbour): the list is the passes' input
+            200: ("density+EOS", (8.0 * d + 8 + 8) * N + 4.0 * nn, 14 * nn + 10 * N),
+            201: ("momentum G11+A", (8.0 * d * 3 + 16) * N + 4.0 * nn, 42 * nn),
             302: ("neighbour-list build", 20.0 * N + 4.0 * nn, 0.0),
             301: ("symplectic integrator", (8.0 * (4 * d + 1) + 8 * 2 * d) * N, 20.0 * N),
             300: ("cell build", (8.0 * d + 8 + 60 + 4 + 16 * (3 * d + 3)) * N, 0.0),

@@ -646,6 +646,16 @@ __device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg,
                     m |= ((mk & 1u) | ((mk >> 15) & 2u)) << (8 * u + 2 * q);
                 }
             }
+            if (q0 == 0 && idx + 1 < ncombo) {
+                // pull the next option's coordinate lines into L1 while this option
+                // is expanded (an L1 miss on a block's loads stalls the whole block)
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    const __half* p = hg.h[a] + nxt.ps;
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+                    if (nxt.ns > 56) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 64));
+                }
+            }
             if (o.ns - q0 < 32) m &= (1u << (o.ns - q0)) - 1u;
             const uint32_t v = (uint32_t)(o.s + q0) | o.icode;
             if (cnt + __popc(m) <= cap) {
