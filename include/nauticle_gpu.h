@@ -237,6 +237,48 @@ nau_status nau_gravity_sources(nau_ctx* ctx, const double* dev_src, long nsrc, l
  * kind: 0 max, 1 min, 2 sum, 3 mean; out has rows*cols doubles (max/min: 1). */
 nau_status nau_reduce(nau_ctx* ctx, int kind, int field_id, double* out);
 
+/* ---- device evaluator for SFL particle-wise arithmetic ----
+ * A register program the host lowers an sfl::ExpressionNode tree to (one
+ * instruction per node, post-order; INTEGRATION.md shows the lowering). Every
+ * register holds one Tensor per particle (rows x cols <= 3 x 3, column-major
+ * components), its shape fixed by the program. Semantics are those of the
+ * reference's Tensor operators (tensor.cpp:43-126) and AST nodes (sfl/ast.cpp:
+ * 71-175): + - need equal shapes; * is scalar scaling or the matrix product
+ * (inner index summed in order); / divides by a scalar or elementwise; ^, min,
+ * max are elementwise with scalar broadcast (std::pow / fmin / fmax);
+ * comparisons take scalars and give 1 or 0; '|' appends a scalar to a column
+ * (<= 3 rows); dot and norm reduce in storage order. Field, constant and
+ * variable references load per-particle or uniform values (LOAD_FIELD /
+ * LOAD_CONST; reductions and interactions are evaluated beforehand into a
+ * uniform value or a field, as the reference freezes / evaluates them). */
+enum {
+    NAU_VM_LOAD_FIELD = 0, /* dst <- field `field` (its shape)          FieldRefNode      */
+    NAU_VM_LOAD_CONST = 1, /* dst <- imm (rows x cols)                   Literal/Constant/Variable */
+    NAU_VM_ADD = 2, NAU_VM_SUB = 3, NAU_VM_MUL = 4, NAU_VM_DIV = 5, NAU_VM_POW = 6,
+    NAU_VM_LT = 7, NAU_VM_GT = 8, NAU_VM_LE = 9, NAU_VM_GE = 10, NAU_VM_EQ = 11, NAU_VM_NE = 12,
+    NAU_VM_NEG = 13,       /* UnaryMinusNode                                                */
+    NAU_VM_JOIN = 14,      /* VectorJoinNode a | b                                          */
+    NAU_VM_EXP = 15, NAU_VM_LOG = 16, NAU_VM_SIN = 17, NAU_VM_COS = 18, NAU_VM_TAN = 19,
+    NAU_VM_SQRT = 20, NAU_VM_ABS = 21, NAU_VM_FLOOR = 22, NAU_VM_SGN = 23, NAU_VM_NORM = 24,
+    NAU_VM_MIN = 25, NAU_VM_MAX = 26, NAU_VM_DOT = 27,
+    NAU_VM_OP_COUNT = 28
+};
+typedef struct {
+    int op;
+    int dst, a, b;       /* registers (a, b: operands; unused ones ignored)      */
+    int field;           /* NAU_VM_LOAD_FIELD                                     */
+    int rows, cols;      /* NAU_VM_LOAD_CONST shape (other ops: derived, ignored) */
+    double imm[9];       /* NAU_VM_LOAD_CONST value, column-major                 */
+} nau_vm_instr;
+enum { NAU_VM_MAX_INSTR = 128, NAU_VM_MAX_REGS = 16 };
+/* out_field = register `result` for every active particle; inactive particles
+ * keep their value (case.cpp:36-40); the output may alias an input field
+ * (two-phase write, case.cpp:31-54). Shape errors fail here with the reference's
+ * message ("operator '+': incompatible shapes 3x1 and 1x1"); a non-finite result
+ * fails at nau_sync with the lowest original index (the NaN audit, case.cpp:46-53). */
+nau_status nau_eval(nau_ctx* ctx, const nau_vm_instr* code, int n_instr, int result,
+                    int out_field);
+
 /* ---- multi-GPU slab decomposition (no reference counterpart:
  * the reference has no domain decomposition) ----
  * Rows are particle-major: every live field in id order (r first), rows x cols

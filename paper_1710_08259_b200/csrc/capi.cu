@@ -350,6 +350,8 @@ void nau_destroy(nau_ctx* c) {
     dfree(c->d_pstart);
     dfree(c->d_pcount);
     dfree(c->d_hesc);
+    if (c->d_vm) cudaFree(c->d_vm);
+    c->d_vm = nullptr;
     if (c->h_err) cudaFreeHost(c->h_err);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

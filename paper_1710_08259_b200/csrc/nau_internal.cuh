@@ -374,6 +374,8 @@ struct nau_ctx {
         int next = 0;
     };
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    void* d_vm = nullptr;  // nau_eval program (vm.cu)
+    size_t vm_len = 0;
     std::vector<IoStage> io_up, io_down;  // indexed by field id
     int mode = NAU_MODE_EXACT;
     int* d_cell_start = nullptr;  // ncells + 2

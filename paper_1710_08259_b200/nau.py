@@ -39,7 +39,7 @@ EXPORTS = [
     "nau_profile_ms", "nau_launch_count", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
     "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows", "nau_dem_step",
     "nau_leapfrog_step", "nau_pack_sources", "nau_gravity_sources", "nau_set_neighbor_lists",
-    "nau_upload_async", "nau_download_async", "nau_io_fence", "nau_io_join",
+    "nau_upload_async", "nau_download_async", "nau_io_fence", "nau_io_join", "nau_eval",
 ]
 
 
@@ -75,6 +75,12 @@ class DemParams(C.Structure):
                 ("f_m", C.c_int), ("R", C.c_double), ("m", C.c_double), ("P", C.c_double),
                 ("Q", C.c_double), ("cf", C.c_double), ("search_radius", C.c_double),
                 ("dt", C.c_double), ("g", C.c_double * 3)]
+
+
+class VmInstr(C.Structure):
+    """nau_vm_instr (include/nauticle_gpu.h): one instruction of a nau_eval program."""
+    _fields_ = [("op", C.c_int), ("dst", C.c_int), ("a", C.c_int), ("b", C.c_int),
+                ("field", C.c_int), ("rows", C.c_int), ("cols", C.c_int), ("imm", C.c_double * 9)]
 
 
 class GravityParams(C.Structure):
@@ -147,6 +153,7 @@ def load():
         "nau_download_async": (i, [vp, i, vp, l]),
         "nau_io_fence": (i, [vp]),
         "nau_io_join": (i, [vp]),
+        "nau_eval": (i, [vp, C.POINTER(VmInstr), i, i, i]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -307,6 +314,17 @@ class Context:
     def download_async(self, f, host_ptr):
         """Asynchronous download into a pinned host buffer (valid after sync())."""
         self._check(self.L.nau_download_async(self.h, self._fid(f), C.c_void_p(host_ptr), self.n))
+
+    def eval_program(self, program, result, out):
+        """≙ one particle-wise SFL equation `out = <program>` (nau_eval). `program` is a
+        list of dicts with keys op, dst, a, b, field, rows, cols, imm (nau_vm_instr)."""
+        arr = (VmInstr * len(program))()
+        for k, ins in enumerate(program):
+            arr[k].op, arr[k].dst, arr[k].a, arr[k].b = ins["op"], ins["dst"], ins["a"], ins["b"]
+            arr[k].field, arr[k].rows, arr[k].cols = ins["field"], ins["rows"], ins["cols"]
+            for q, v in enumerate(ins["imm"]):
+                arr[k].imm[q] = v
+        self._check(self.L.nau_eval(self.h, arr, len(program), result, self._fid(out)))
 
     def io_fence(self):
         self._check(self.L.nau_io_fence(self.h))

@@ -410,6 +410,101 @@ def test_neighbor_lists_capacity_growth_and_fallback(n, radius, kind, outside):
             np.testing.assert_array_equal(on[k], off[k], err_msg=(fast, k))
 
 
+# ------------------------------------------- device SFL evaluator (§8(f) 1) ----
+def _vm_context():
+    import sfl_mini
+    z = np.load(os.path.join(GOLD, "vm_cases.npz"))
+    meta = json.loads(str(z["meta"]))
+    c = nau.Context(0)
+    c.set_domain(3, [0, 0, 0], [2, 2, 2], [0.5, 0.5, 0.5], [nau.CUTOFF] * 3)
+    c.set_particles(z["pos"])
+    for k, (r, cc) in meta["shapes"].items():
+        c.add_field(k, r, cc, z["f_" + k])
+    for k, r in (("o1", 1), ("o2", 2), ("o3", 3)):
+        c.add_field(k, r, 1, 0.0)
+    c.add_field("o9", 3, 3, 0.0)
+    sym = {k: ("field", c.fields[k].id) for k in meta["shapes"]}
+    sym.update({k: ("const", np.array(v)) for k, v in meta["consts"].items()})
+    return z, meta, c, sym, sfl_mini
+
+
+def test_vm_expressions_vs_reference():
+    """50 particle-wise SFL expressions (every operator, builtin and shape rule) through
+    nau_eval vs the reference's own parser + AST evaluation: bitwise without a libm
+    transcendental, within 1e-14 with one (CUDA vs glibc exp/log/sin/cos/tan/pow)."""
+    z, meta, c, sym, sfl_mini = _vm_context()
+    try:
+        for idx, expr in enumerate(meta["expressions"]):
+            want = z[f"e{idx}"]
+            out = {1: "o1", 2: "o2", 3: "o3", 9: "o9"}[want.shape[0]]
+            prog, res = sfl_mini.lower(expr, sym)
+            c.eval_program(prog, res, out)
+            got = c.download(out)
+            if sfl_mini.uses_transcendental(expr):
+                np.testing.assert_allclose(got, want, rtol=1e-14, atol=1e-300, err_msg=expr)
+            else:
+                np.testing.assert_array_equal(got, want, err_msg=expr)
+    finally:
+        c.close()
+
+
+def test_vm_shape_errors_and_nan_audit():
+    z, meta, c, sym, sfl_mini = _vm_context()
+    try:
+        msgs = json.loads(str(z["error_messages"]))
+        for expr, ref_msg in zip(meta["errors"], msgs):
+            prog, res = sfl_mini.lower(expr, sym)
+            with pytest.raises(nau.NauError) as ei:
+                c.eval_program(prog, res, "o9")
+            assert ei.value.status == 1, expr  # NAU_ERR_RUNTIME
+            assert ref_msg.startswith(ei.value.message), (expr, ei.value.message, ref_msg)
+        # wrong LHS shape (case.cpp:41-44)
+        prog, res = sfl_mini.lower("u", sym)
+        with pytest.raises(nau.NauError, match="LHS field is 1x1 but RHS produced 3x1"):
+            c.eval_program(prog, res, "o1")
+        # NaN audit (case.cpp:46-53): log of a negative value, lowest original index
+        prog, res = sfl_mini.lower("log(t)", sym)
+        t = z["f_t"][0]
+        with pytest.raises(nau.NauError) as ei:
+            c.eval_program(prog, res, "o1")
+            c.sync()
+        assert ei.value.status == 2 and ei.value.particle == int(np.flatnonzero(t <= 0)[0])
+    finally:
+        c.close()
+
+
+def test_vm_two_phase_and_inactive():
+    """out may alias an operand (two-phase write); particles outside a cut-off
+    domain are inactive and keep their value (case.cpp:36-40)."""
+    z, meta, c, sym, sfl_mini = _vm_context()
+    try:
+        s0 = c.download("s").copy()
+        t0 = c.download("t").copy()
+        prog, res = sfl_mini.lower("s*s+t", sym)
+        c.eval_program(prog, res, "s")
+        np.testing.assert_array_equal(c.download("s"), s0 * s0 + t0)
+    finally:
+        c.close()
+    c = nau.Context(0)
+    try:
+        pos = z["pos"].copy()
+        pos[0, 7] = 1.5  # outside the [0, 1] cut-off box: deactivated by the shift
+        c.set_domain(3, [0, 0, 0], [2, 2, 2], [0.5, 0.5, 0.5], [nau.CUTOFF] * 3)
+        c.set_particles(pos)
+        c.add_field("s", 1, 1, z["f_s"])
+        c.add_field("o1", 1, 1, -7.0)
+        c.boundary_shift()
+        import sfl_mini
+        prog, res = sfl_mini.lower("2*s", {"s": ("field", c.fields["s"].id)})
+        c.eval_program(prog, res, "o1")
+        got = c.download("o1")[0]
+        want = 2 * z["f_s"][0]
+        want[7] = -7.0
+        np.testing.assert_array_equal(got, want)
+    finally:
+        c.close()
+
+
 def test_async_host_io_matches_sync():
     """nau_upload_async / nau_download_async (double-buffered staging on copy
     streams) give the same per-step results as the synchronous calls."""
