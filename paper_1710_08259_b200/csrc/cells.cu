@@ -266,7 +266,9 @@ __global__ void k_half_coords(DomainDev d, long n, const double* pos, const int*
         const int ca = rem % d.cells[a];
         rem /= d.cells[a];
         const double q = (pos[a * n + k] - d.lo[a]) / d.cs[a] - (double)ca;
-        esc |= !(q >= -1e-3 && q <= 1.001);
+        // in its cell (floor == cell index) q lies in [0, 1): the fp16 bound of
+        // sweep.cuh HalfGrid assumes |h| <= 1; anything else disables the fp16 path
+        esc |= !(q >= 0.0 && q <= 1.0);
         h[a * hlen + p] = __double2half(q);  // round to nearest
     }
     if (esc) atomicOr(escaped, 1);
