@@ -88,18 +88,19 @@ nau_status nau_create(int device, nau_ctx** out);
 void nau_destroy(nau_ctx* ctx);
 
 /* Evaluation mode of the neighbour sums.
- * EXACT (default): one lane per particle, candidates summed in the reference's
- *   order with the reference's arithmetic (no FMA, IEEE div/sqrt): bitwise equal
- *   to the reference wherever no libm transcendental is involved.
- * FAST: one warp per particle, FMA/rsqrt/reciprocal arithmetic and a warp-tree
- *   reduction: same candidates and filters, summation order differs
- *   (BASELINE tolerance: 1e-10 relative; observed ~1e-14). */
+ * EXACT (default): candidates summed in the reference's order with the
+ *   reference's arithmetic (no FMA, IEEE div/sqrt): bitwise equal to the
+ *   reference wherever no libm transcendental is involved.
+ * FAST: same candidates, filters and error checks, FMA/rsqrt/reciprocal
+ *   arithmetic and a balanced candidate order (BASELINE tolerance: 1e-10
+ *   relative; observed ~1e-14). */
 enum { NAU_MODE_EXACT = 0, NAU_MODE_FAST = 1 };
 nau_status nau_set_mode(nau_ctx* ctx, int mode);
 int nau_get_mode(nau_ctx* ctx);
-/* Per-step neighbour lists for nau_wcsph_step (default on): the cell sweep runs
- * once per step and both passes read its list; same candidates in the same
- * order, so results are identical either way. Off = each pass sweeps itself. */
+/* Neighbour lists (default on): the candidate scan runs once per cell build and
+ * every SPH operator with a uniform radius (nau_interact, nau_wcsph_step) reads
+ * the list; same candidates in the same order, so results are identical either
+ * way. Off = each pass sweeps the cells itself. */
 nau_status nau_set_neighbor_lists(nau_ctx* ctx, int on);
 /* Use an external CUDA stream (cudaStream_t), e.g. torch's current stream. NULL = own stream. */
 nau_status nau_set_stream(nau_ctx* ctx, void* stream);
@@ -261,7 +262,8 @@ enum {
     NAU_VM_EXP = 15, NAU_VM_LOG = 16, NAU_VM_SIN = 17, NAU_VM_COS = 18, NAU_VM_TAN = 19,
     NAU_VM_SQRT = 20, NAU_VM_ABS = 21, NAU_VM_FLOOR = 22, NAU_VM_SGN = 23, NAU_VM_NORM = 24,
     NAU_VM_MIN = 25, NAU_VM_MAX = 26, NAU_VM_DOT = 27,
-    NAU_VM_OP_COUNT = 28
+    NAU_VM_RAND = 28,      /* RandNode rand(a, b): RandomState::uniform(i, a, b)        */
+    NAU_VM_OP_COUNT = 29
 };
 typedef struct {
     int op;
@@ -278,6 +280,14 @@ enum { NAU_VM_MAX_INSTR = 128, NAU_VM_MAX_REGS = 16 };
  * fails at nau_sync with the lowest original index (the NaN audit, case.cpp:46-53). */
 nau_status nau_eval(nau_ctx* ctx, const nau_vm_instr* code, int n_instr, int result,
                     int out_field);
+/* ≙ the case's RandomState (sfl/random_state.hpp): every `rand` draw is a pure
+ * function of (seed, original particle index, that particle's draw counter).
+ * counters: n values in original order, or NULL for zeros (a fresh case). The
+ * counters persist across nau_eval calls like the reference's (hot start writes
+ * them back, scheduler.cpp:47-54). */
+nau_status nau_set_random_state(nau_ctx* ctx, unsigned long long seed,
+                                const unsigned long long* counters);
+nau_status nau_get_random_counters(nau_ctx* ctx, unsigned long long* counters);
 
 /* ---- multi-GPU slab decomposition (no reference counterpart:
  * the reference has no domain decomposition) ----

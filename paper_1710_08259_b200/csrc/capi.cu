@@ -173,6 +173,7 @@ const char* msg_text(int msg) {
         case nau::kMsgOutsideCutoff: return "particle outside the domain on a cut-off axis";
         case nau::kMsgCoincident: return "nbody_gravity: coincident particles with zero softening";
         case nau::kMsgDemParams: return "dem contact: nonpositive Young modulus or radius";
+        case nau::kMsgRandBounds: return "rand: lower bound exceeds upper bound";
         default: return "runtime error";
     }
 }
@@ -352,6 +353,7 @@ void nau_destroy(nau_ctx* c) {
     dfree(c->d_hesc);
     if (c->d_vm) cudaFree(c->d_vm);
     c->d_vm = nullptr;
+    dfree(c->d_rng);
     if (c->h_err) cudaFreeHost(c->h_err);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -433,6 +435,8 @@ nau_status nau_set_particles(nau_ctx* c, long n, const double* pos_soa) {
     }
     cudaStreamSynchronize(c->stream);
     free_particles(c);
+    dfree(c->d_rng);  // a new particle set starts a fresh RandomState
+    c->rng_len = 0;
     c->n = n;
     nau_status sa = nau::alloc_particle_arrays(c, n);
     if (sa != NAU_OK) return sa;

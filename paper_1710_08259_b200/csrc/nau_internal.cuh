@@ -51,6 +51,7 @@ enum ErrMsg {
     kMsgCoincident = 4,
     kMsgDemParams = 5,
     kMsgNan = 6,
+    kMsgRandBounds = 7,
 };
 
 // Operand as seen by a kernel: field pointer (cell order) or uniform value.
@@ -376,6 +377,9 @@ struct nau_ctx {
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     void* d_vm = nullptr;  // nau_eval program (vm.cu)
     size_t vm_len = 0;
+    unsigned long long* d_rng = nullptr;  // RandomState counters, original order (vm.cu)
+    long rng_len = 0;
+    unsigned long long rng_seed = 0;
     std::vector<IoStage> io_up, io_down;  // indexed by field id
     int mode = NAU_MODE_EXACT;
     int* d_cell_start = nullptr;  // ncells + 2

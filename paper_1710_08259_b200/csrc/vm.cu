@@ -60,10 +60,21 @@ __device__ __forceinline__ double vm_binary(int op, double x, double y) {
     }
 }
 
+// RandomState::uniform (sfl/random_state.hpp): splitmix64-style mixing of (seed,
+// particle, per-particle counter), 53 random bits.
+__device__ __forceinline__ unsigned long long rng_mix(unsigned long long x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
 __global__ void __launch_bounds__(kVmThreads) k_vm(const VmIns* __restrict__ prog, int nins,
                                                    int result, long n, VmFields f,
                                                    const uint8_t* active, const int* orig,
-                                                   double* out, DevErr* err) {
+                                                   double* out, DevErr* err,
+                                                   unsigned long long* rng, long rng_len,
+                                                   unsigned long long seed) {
     const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (k >= n || !active[k]) return;  // inactive particles keep their value (case.cpp:36-40)
     double R[NAU_VM_MAX_REGS][9];
@@ -137,6 +148,23 @@ __global__ void __launch_bounds__(kVmThreads) k_vm(const VmIns* __restrict__ pro
                 d[I.ar] = tail;
                 break;
             }
+            case NAU_VM_RAND: {  // RandNode (sfl/ast.cpp:212-217)
+                const double lo = a[0], hi = b[0];
+                if (lo > hi) {
+                    latch_error(err, 1, kMsgRandBounds, orig[k]);
+                    d[0] = 0.0;
+                    break;
+                }
+                const long i = orig[k];
+                const long slot = i < rng_len ? i : 0;
+                const unsigned long long cnt = rng[slot]++;  // one thread per particle
+                const unsigned long long x =
+                    rng_mix(rng_mix(seed ^ 0x6e61757469636c65ULL) ^
+                            rng_mix((unsigned long long)slot + 0x9e3779b9ULL) ^ cnt);
+                const double u = (double)(x >> 11) * 0x1.0p-53;
+                d[0] = lo + u * (hi - lo);
+                break;
+            }
             case NAU_VM_NORM: {  // sqrt(squaredNorm()), storage order
                 const int m = I.ar * I.ac;
                 double s = a[0] * a[0];
@@ -208,6 +236,7 @@ static bool vm_compile(nau_ctx* c, const nau_vm_instr* code, int n, int result, 
             return false;
         }
         const bool unary = in.op == NAU_VM_NEG || (in.op >= NAU_VM_EXP && in.op <= NAU_VM_NORM);
+        // (NAU_VM_RAND is binary: the two bounds)
         const bool loads = in.op == NAU_VM_LOAD_FIELD || in.op == NAU_VM_LOAD_CONST;
         if (!loads && (bad_reg(in.a) || !def[in.a] || (!unary && (bad_reg(in.b) || !def[in.b])))) {
             err = "nau_eval: instruction " + std::to_string(pc) + " reads an undefined register";
@@ -284,6 +313,13 @@ static bool vm_compile(nau_ctx* c, const nau_vm_instr* code, int n, int result, 
             case NAU_VM_NORM:
                 D = {1, 1};
                 break;
+            case NAU_VM_RAND:  // Tensor::value() on both bounds (tensor.hpp:50-53)
+                if (!A.scalar() || !B.scalar()) {
+                    err = "expected a scalar, got a " + shape_str(A.scalar() ? B : A) + " tensor";
+                    return false;
+                }
+                D = {1, 1};
+                break;
             case NAU_VM_DOT:  // tensor.cpp:107-110
                 if (A.rows != B.rows || A.cols != B.cols) return mismatch("dot");
                 D = {1, 1};
@@ -316,7 +352,8 @@ static void launch_vm(nau_ctx* c, const VmIns* d_prog, int nins, int result, dou
     for (size_t q = 0; q < c->fields.size() && q < (size_t)kMaxFields; ++q) f.p[q] = c->fields[q].d;
     const int blocks = (int)((c->n + kVmThreads - 1) / kVmThreads);
     k_vm<<<blocks, kVmThreads, 0, c->stream>>>(d_prog, nins, result, c->n, f, c->d_active,
-                                               c->d_orig, out, c->d_err);
+                                               c->d_orig, out, c->d_err, c->d_rng, c->rng_len,
+                                               c->rng_seed);
     c->launches++;
 }
 
@@ -373,11 +410,58 @@ extern "C" nau_status nau_eval(nau_ctx* c, const nau_vm_instr* code, int n_instr
                         c->stream);
         out = of.alt;
     }
+    bool uses_rand = false;
+    for (int pc = 0; pc < n_instr; ++pc) uses_rand |= code[pc].op == NAU_VM_RAND;
+    if (uses_rand && c->rng_len < c->n) {  // a fresh RandomState: zero counters
+        nau_status s = nau_set_random_state(c, c->rng_seed, nullptr);
+        if (s != NAU_OK) return s;
+    }
     nau::launch_vm(c, static_cast<const nau::VmIns*>(c->d_vm), n_instr, result, out);
     if (alias) std::swap(of.d, of.alt);
     if (out_field == 0) {  // r written: apply_boundary_shift + dirty (case.cpp:59-62)
         nau::launch_boundary_shift(c);
         c->dirty = true;
+    }
+    return NAU_OK;
+}
+
+extern "C" nau_status nau_set_random_state(nau_ctx* c, unsigned long long seed,
+                                           const unsigned long long* counters) {
+    c->rng_seed = seed;
+    if (c->rng_len < c->n) {
+        if (c->d_rng) cudaFree(c->d_rng);
+        c->d_rng = nullptr;
+        c->rng_len = 0;
+        if (c->n > 0 && cudaMalloc(&c->d_rng, sizeof(unsigned long long) * c->n) != cudaSuccess) {
+            c->last_error = "nau_set_random_state: device allocation failed";
+            return NAU_ERR_CUDA;
+        }
+        c->rng_len = c->n;
+    }
+    if (c->n == 0) return NAU_OK;
+    const size_t bytes = sizeof(unsigned long long) * c->n;
+    cudaError_t e = counters ? cudaMemcpyAsync(c->d_rng, counters, bytes, cudaMemcpyHostToDevice, c->stream)
+                             : cudaMemsetAsync(c->d_rng, 0, bytes, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+        c->last_error = cudaGetErrorString(e);
+        return NAU_ERR_CUDA;
+    }
+    return NAU_OK;
+}
+
+extern "C" nau_status nau_get_random_counters(nau_ctx* c, unsigned long long* counters) {
+    if (c->n == 0) return NAU_OK;
+    if (c->rng_len < c->n) {  // never drawn: zeros
+        for (long i = 0; i < c->n; ++i) counters[i] = 0;
+        return NAU_OK;
+    }
+    cudaError_t e = cudaMemcpyAsync(counters, c->d_rng, sizeof(unsigned long long) * c->n,
+                                    cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+        c->last_error = cudaGetErrorString(e);
+        return NAU_ERR_CUDA;
     }
     return NAU_OK;
 }

@@ -40,6 +40,7 @@ EXPORTS = [
     "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows", "nau_dem_step",
     "nau_leapfrog_step", "nau_pack_sources", "nau_gravity_sources", "nau_set_neighbor_lists",
     "nau_upload_async", "nau_download_async", "nau_io_fence", "nau_io_join", "nau_eval",
+    "nau_set_random_state", "nau_get_random_counters",
 ]
 
 
@@ -154,6 +155,8 @@ def load():
         "nau_io_fence": (i, [vp]),
         "nau_io_join": (i, [vp]),
         "nau_eval": (i, [vp, C.POINTER(VmInstr), i, i, i]),
+        "nau_set_random_state": (i, [vp, C.c_ulonglong, vp]),
+        "nau_get_random_counters": (i, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -325,6 +328,19 @@ class Context:
             for q, v in enumerate(ins["imm"]):
                 arr[k].imm[q] = v
         self._check(self.L.nau_eval(self.h, arr, len(program), result, self._fid(out)))
+
+    def set_random_state(self, seed, counters=None):
+        """≙ the case's RandomState: seed + per-particle draw counters (original order)."""
+        ptr = None
+        if counters is not None:
+            self._rng_keep = np.ascontiguousarray(counters, dtype=np.uint64)
+            ptr = _p(self._rng_keep)
+        self._check(self.L.nau_set_random_state(self.h, C.c_ulonglong(seed), ptr))
+
+    def random_counters(self):
+        out = np.zeros(self.n, dtype=np.uint64)
+        self._check(self.L.nau_get_random_counters(self.h, _p(out)))
+        return out
 
     def io_fence(self):
         self._check(self.L.nau_io_fence(self.h))

@@ -35,7 +35,12 @@ EXPRESSIONS = [
     "max(M,N)", "dot(u,w)", "dot(M,N)", "dot(u,cv)", "c*u+cv", "M*(u+w)-N*u",
 ]
 
-ERRORS = ["u+s", "s-u", "u*w", "s/u", "u^M", "u<s", "u|s", "(t|s|c)|s", "dot(u,s)", "M*w|s"]
+# rand(a, b): evaluated on a fresh case each (zero draw counters), the last one twice
+# on the same case (the counters persist: the second draw differs)
+RAND_EXPRESSIONS = ["rand(0,1)", "s*rand(-1,1)+rand(t-1,t+1)", "rand(0,s)|t"]
+
+ERRORS = ["u+s", "s-u", "u*w", "s/u", "u^M", "u<s", "u|s", "(t|s|c)|s", "dot(u,s)", "M*w|s",
+          "rand(u,s)"]
 
 
 def make_case(seed=4242):
@@ -64,7 +69,8 @@ def main():
         rc.constant(k, v)
     out = {"pos": pos, "meta": np.array(json.dumps({
         "shapes": shapes, "consts": {k: v.tolist() for k, v in consts.items()},
-        "expressions": EXPRESSIONS, "errors": ERRORS}))}
+        "expressions": EXPRESSIONS, "errors": ERRORS, "rand": RAND_EXPRESSIONS,
+        "rand_seed": 7}))}
     for k, v in fields.items():
         out["f_" + k] = v
     import sfl_mini
@@ -76,6 +82,15 @@ def main():
         fl = {j: (shapes[k][0], shapes[k][1], fields[k]) for j, k in enumerate(fields)}
         comps = sfl_mini.run_numpy(prog, res, fl, N).shape[0]
         out[f"e{idx}"] = rc.eval(e, comps)
+    for idx, e in enumerate(RAND_EXPRESSIONS):
+        rr = ref.RefCase(3, [0, 0, 0], [2, 2, 2], [0.5, 0.5, 0.5], [2, 2, 2], pos, seed=7)
+        for k, v in fields.items():
+            rows, cols = shapes[k]
+            rr.field(k, v, rows=rows, cols=cols)
+        comps = 2 if "|" in e else 1
+        out[f"r{idx}"] = rr.eval(e, comps)
+        if idx == len(RAND_EXPRESSIONS) - 1:
+            out[f"r{idx}_again"] = rr.eval(e, comps)
     msgs = []
     for e in ERRORS:
         try:

@@ -21,10 +21,10 @@ import numpy as np
 # opcodes (include/nauticle_gpu.h NAU_VM_*)
 OPS = ["LOAD_FIELD", "LOAD_CONST", "ADD", "SUB", "MUL", "DIV", "POW", "LT", "GT", "LE", "GE",
        "EQ", "NE", "NEG", "JOIN", "EXP", "LOG", "SIN", "COS", "TAN", "SQRT", "ABS", "FLOOR",
-       "SGN", "NORM", "MIN", "MAX", "DOT"]
+       "SGN", "NORM", "MIN", "MAX", "DOT", "RAND"]
 OP = {name: k for k, name in enumerate(OPS)}
 UNARY = {"exp", "log", "sin", "cos", "tan", "sqrt", "abs", "floor", "sgn", "norm"}
-BINARY = {"min", "max", "dot"}
+BINARY = {"min", "max", "dot", "rand"}
 CMP = {"<": "LT", ">": "GT", "<=": "LE", ">=": "GE", "==": "EQ", "!=": "NE"}
 TRANSCENDENTAL = {"exp", "log", "sin", "cos", "tan", "^"}
 
@@ -228,12 +228,35 @@ def uses_transcendental(text):
 
 
 # ------------------------------------------------------- host interpreter ----
-def run_numpy(prog, result, fields, n):
+M64 = (1 << 64) - 1
+
+
+def _mix(x):
+    x = (x + 0x9E3779B97F4A7C15) & M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M64
+    return x ^ (x >> 31)
+
+
+def rand_uniform(seed, counters, a, b):
+    """RandomState::uniform (sfl/random_state.hpp) for particles 0..n-1; advances counters."""
+    out = np.empty(len(counters))
+    s0 = _mix(seed ^ 0x6E61757469636C65)
+    for i in range(len(counters)):
+        x = _mix(s0 ^ _mix(i + 0x9E3779B9) ^ int(counters[i]))
+        counters[i] += 1
+        u = float(x >> 11) * 2.0 ** -53
+        out[i] = a[i] + u * (b[i] - a[i])
+    return out
+
+
+def run_numpy(prog, result, fields, n, seed=0, counters=None):
+    counters = np.zeros(n, dtype=np.uint64) if counters is None else counters
     with np.errstate(all="ignore"):
-        return _run_numpy(prog, result, fields, n)
+        return _run_numpy(prog, result, fields, n, seed, counters)
 
 
-def _run_numpy(prog, result, fields, n):
+def _run_numpy(prog, result, fields, n, seed, counters):
     """Evaluate a program for n particles on the host. fields: id -> (rows, cols, soa
     (rows*cols, n) column-major components). Returns (rows*cols, n)."""
     regs = {}
@@ -297,6 +320,8 @@ def _run_numpy(prog, result, fields, n):
             regs[d] = (1, 1, f(a[0], b[0]).astype(np.float64)[None, :])
         elif op == "JOIN":
             regs[d] = (ar + 1, 1, np.concatenate([a, b[:1]], axis=0))
+        elif op == "RAND":
+            regs[d] = (1, 1, rand_uniform(seed, counters, a[0], b[0])[None, :])
         elif op == "DOT":
             s = a[0] * b[0]
             for c in range(1, ar * ac):

@@ -444,6 +444,19 @@ def test_vm_expressions_vs_reference():
                 np.testing.assert_allclose(got, want, rtol=1e-14, atol=1e-300, err_msg=expr)
             else:
                 np.testing.assert_array_equal(got, want, err_msg=expr)
+        # rand: the reference's RandomState, fresh counters per expression; the last
+        # expression drawn twice (counters persist across evaluations)
+        for idx, expr in enumerate(meta["rand"]):
+            c.set_random_state(meta["rand_seed"])
+            want = z[f"r{idx}"]
+            out = {1: "o1", 2: "o2"}[want.shape[0]]
+            prog, res = sfl_mini.lower(expr, sym)
+            c.eval_program(prog, res, out)
+            np.testing.assert_array_equal(c.download(out), want, err_msg=expr)
+            if f"r{idx}_again" in z:
+                c.eval_program(prog, res, out)
+                np.testing.assert_array_equal(c.download(out), z[f"r{idx}_again"], err_msg=expr)
+                assert (c.random_counters() == 2).all()
     finally:
         c.close()
 

@@ -53,3 +53,20 @@ def test_error_cases_are_reference_errors():
     z, meta, fields, sym = _load()
     msgs = json.loads(str(z["error_messages"]))
     assert all(m for m in msgs), msgs  # every listed program is rejected by the reference
+
+
+def test_rand_matches_reference_random_state():
+    """rand(a, b) = RandomState::uniform(i, a, b) with per-particle draw counters
+    (sfl/random_state.hpp); counters persist across evaluations."""
+    z, meta, fields, sym = _load()
+    n = z["pos"].shape[1]
+    seed = meta["rand_seed"]
+    for idx, expr in enumerate(meta["rand"]):
+        prog, res = sfl_mini.lower(expr, sym)
+        counters = np.zeros(n, dtype=np.uint64)
+        got = sfl_mini.run_numpy(prog, res, fields, n, seed=seed, counters=counters)
+        np.testing.assert_array_equal(got, z[f"r{idx}"], err_msg=expr)
+        if f"r{idx}_again" in z:
+            got2 = sfl_mini.run_numpy(prog, res, fields, n, seed=seed, counters=counters)
+            np.testing.assert_array_equal(got2, z[f"r{idx}_again"], err_msg=expr)
+            assert not np.array_equal(got2, got)
