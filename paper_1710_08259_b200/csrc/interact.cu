@@ -401,6 +401,84 @@ __global__ void __launch_bounds__(kGravTile) k_gravity(const __grid_constant__ G
     }
 }
 
+// FAST, uniform G, uniform eps > 0 (the BASELINE cfg4 deck): every thread sums
+// kGravBodies bodies against each staged source, the source tile holds
+// (x, y, z, G m_j) with G m_j = 0 for inactive sources, and the self pair needs no
+// test: rel = 0 there, so it adds exactly zero (r2 = eps^2 > 0 keeps it finite).
+// Per pair: 3 DADD + 3 DFMA + rsqrt + 3 DMUL + 3 DFMA and a quarter of a shared
+// load — profiles/r1b: the one-body loop issued 45 instructions per pair.
+constexpr int kGravBodies = 2;
+constexpr int kGravThreads = 128;
+
+template <int DIM>
+__global__ void __launch_bounds__(kGravThreads) k_gravity_fast(const __grid_constant__ GravArgs a,
+                                                               double G, double eps2) {
+    __shared__ double4 s4[kGravTile];
+    const long n = a.n;
+    const long k0 = (long)blockIdx.x * (kGravThreads * kGravBodies) + threadIdx.x;
+    double xi[kGravBodies][3], acc[kGravBodies][3];
+#pragma unroll
+    for (int b = 0; b < kGravBodies; ++b) {
+        const long k = k0 + b * kGravThreads;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            xi[b][d] = (d < DIM && k < n) ? a.x[d * n + k] : 0.0;
+            acc[b][d] = 0.0;
+        }
+    }
+    const long ns = a.src ? a.nsrc : n;
+    for (long base = 0; base < ns; base += kGravTile) {
+        for (int t = threadIdx.x; t < kGravTile; t += kGravThreads) {
+            const long j = base + t;
+            double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+            if (j < ns) {
+                if (a.src) {
+                    v = a.src[j];
+                    v.w = G * v.w;  // m = 0 marks an inactive source
+                } else {
+                    double xs[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+                    for (int d = 0; d < DIM; ++d) xs[d] = a.x[d * n + j];
+                    v = make_double4(xs[0], xs[1], xs[2], a.active[j] ? G * a.m.at(0, (int)j, n) : 0.0);
+                }
+            }
+            s4[t] = v;
+        }
+        __syncthreads();
+        const int lim = (int)min((long)kGravTile, ns - base);
+#pragma unroll 2
+        for (int t = 0; t < lim; ++t) {
+            const double4 sj = s4[t];
+            const double xj[3] = {sj.x, sj.y, sj.z};
+#pragma unroll
+            for (int b = 0; b < kGravBodies; ++b) {
+                double rel[3] = {0.0, 0.0, 0.0};
+                double r2 = eps2;
+#pragma unroll
+                for (int d = DIM - 1; d >= 0; --d) {
+                    rel[d] = xj[d] - xi[b][d];
+                    r2 = fma(rel[d], rel[d], r2);
+                }
+                const double inv = rsqrt(r2);
+                const double s = sj.w * (inv * (inv * inv));
+#pragma unroll
+                for (int d = 0; d < DIM; ++d) acc[b][d] = fma(rel[d], s, acc[b][d]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int b = 0; b < kGravBodies; ++b) {
+        const long k = k0 + b * kGravThreads;
+        if (k >= n || !a.active[k]) continue;  // inactive bodies keep their value
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+            if (!isfinite(acc[b][d])) latch_error(a.err, 2, kMsgNan, a.orig[k]);
+            a.out[d * n + k] = acc[b][d];
+        }
+    }
+}
+
 template <int DIM, int OP, int KF>
 void sph_launch(nau_ctx* c, const SphArgs& a, int ac) {
     const int blocks = (int)((c->n + kThreads - 1) / kThreads);
@@ -490,7 +568,15 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
         const int blocks = (int)((c->n + kGravTile - 1) / kGravTile);
         prof_begin(c, 100 + op);
         const bool fast = c->mode == NAU_MODE_FAST;
-        if (dim == 1) {
+        const bool uniform_soft = a.G.p == nullptr && a.has_eps && a.eps.p == nullptr &&
+                                  a.eps.v[0] * a.eps.v[0] > 0.0;
+        if (fast && uniform_soft) {
+            const int nb = (int)((c->n + kGravThreads * kGravBodies - 1) / (kGravThreads * kGravBodies));
+            const double G = a.G.v[0], eps2 = a.eps.v[0] * a.eps.v[0];
+            if (dim == 1) k_gravity_fast<1><<<nb, kGravThreads, 0, c->stream>>>(a, G, eps2);
+            else if (dim == 2) k_gravity_fast<2><<<nb, kGravThreads, 0, c->stream>>>(a, G, eps2);
+            else k_gravity_fast<3><<<nb, kGravThreads, 0, c->stream>>>(a, G, eps2);
+        } else if (dim == 1) {
             if (fast) k_gravity<1, true><<<blocks, kGravTile, 0, c->stream>>>(a);
             else k_gravity<1, false><<<blocks, kGravTile, 0, c->stream>>>(a);
         } else if (dim == 2) {

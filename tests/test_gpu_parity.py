@@ -674,11 +674,13 @@ def test_dem_deck_vs_port(ctx, fast):
     ctx.set_mode(False)
 
 
-def test_gravity_leapfrog_vs_port(ctx):
+@pytest.mark.parametrize("fast", [False, True])
+def test_gravity_leapfrog_vs_port(ctx, fast):
     """cfg4 deck on N = 1024 Plummer bodies: 3 leapfrog steps within 1e-10 (pow vs r^1.5);
-    total momentum stays ~0."""
+    total momentum stays ~0. FAST runs the multi-body kernel (uniform G, eps > 0)."""
     sc = scenes.plummer(n=1024)
     prm = sc.params
+    ctx.set_mode(fast)
     ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
     ctx.set_particles(sc.pos)
     ctx.add_field("v", 3, 1, sc.fields["v"])
@@ -706,6 +708,7 @@ def test_gravity_leapfrog_vs_port(ctx):
     assert rel_err(ctx.download("a"), a) <= TOL_STEP
     mom = ctx.download("v").sum(axis=1) * prm["m"]
     assert np.abs(mom).max() <= 1e-12
+    ctx.set_mode(False)
 
 
 @pytest.mark.parametrize("fast", [False, True])
