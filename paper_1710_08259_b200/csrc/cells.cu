@@ -232,16 +232,17 @@ __global__ void __launch_bounds__(kSweepThreads) k_nlist(const __grid_constant__
                                                          int* over, const __grid_constant__ HalfGrid hg) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= *g.nact) return;
-    uint32_t* lst = list + nlist_base(k, cap);
+    uint2* lst = reinterpret_cast<uint2*>(list) + nlist_base(k, cap);
     const float pre_r = (float)radius;
-    int cnt;
+    int cnt, nrec = 0;
     if (hg.on && *hg.escaped == 0)
-        cnt = build_list_half<DIM, ORDERED>(g, hg, k, lst, cap);
+        cnt = build_list_half<DIM, ORDERED>(g, hg, k, lst, cap, nrec);
     else
-        cnt = axis_mode(g, radius) < 2 ? build_list<DIM, ORDERED, false>(g, xl, k, pre_r, lst, cap)
-                                       : build_list<DIM, ORDERED, true>(g, xl, k, pre_r, lst, cap);
-    count[k] = min(cnt, cap);
-    if (cnt > cap) atomicMax(over, cnt);
+        cnt = axis_mode(g, radius) < 2
+                  ? build_list<DIM, ORDERED, false>(g, xl, k, pre_r, lst, cap, nrec)
+                  : build_list<DIM, ORDERED, true>(g, xl, k, pre_r, lst, cap, nrec);
+    count[k] = cnt;
+    if (nrec > cap) atomicMax(over, nrec);
 }
 
 // fp16 cell-relative coordinates (sweep.cuh HalfGrid): padded cell sizes, then one
@@ -425,7 +426,7 @@ static HalfGrid half_grid(nau_ctx* c, double radius) {
 bool build_nlist(nau_ctx* c, double radius, bool ordered) {
     const long n = c->n;
     if (n == 0 || !c->use_nlist) return false;
-    constexpr int kMaxCap = 4096;  // beyond this the lists would cost more than they save
+    constexpr int kMaxCap = 1024;  // records per slot; beyond this sweeping is cheaper
     const size_t slots = (size_t)((n + 31) / 32) * 32;
     if (c->nl_cap == 0) c->nl_cap = 64;
     if (!c->d_nover && cudaMalloc(&c->d_nover, sizeof(int)) != cudaSuccess) return false;
@@ -441,7 +442,8 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered) {
     const int b = blocks_for(n, T);
     const HalfGrid hg = half_grid(c, radius);
     for (int attempt = 0; attempt < 3; ++attempt) {
-        const size_t need = slots * (size_t)c->nl_cap;
+        // uint2 records + one slack row (consume_list reads one record ahead)
+        const size_t need = slots * (size_t)c->nl_cap * 2 + 64;
         if (c->nl_len < need) {
             if (c->d_nlist) cudaFree(c->d_nlist);
             c->d_nlist = nullptr;

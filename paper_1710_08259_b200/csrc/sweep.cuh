@@ -287,29 +287,42 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
 
 // ---- per-step neighbour lists (used by the two-pass WCSPH deck) --------------
 // The density and momentum passes of a step walk the same candidates, so the
-// scan phase runs once (k_nlist) and stores every pre-filter survivor, in
-// candidate order, into a lane-interleaved list: entry s of slot k lives at
-// list[((k/32)*cap + s)*32 + k%32] (coalesced for a warp). The passes then only
-// consume their list (consume_list). Same order as the sweep => same sums.
+// scan phase runs once (k_nlist) and stores the pre-filter survivors, in
+// candidate order, as CHUNK RECORDS: one (base, mask) pair of u32 per block of
+// 32 consecutive candidate slots with at least one survivor — base = first slot
+// | image code << kSlotBits, bit b of mask = slot base + b survives. Record r of
+// slot k lives at rec[((k/32)*cap + r)*32 + k%32] (coalesced 256 B per warp).
+// The consumers expand the masks on the fly (consume_list), so they visit the
+// same candidates in the same order as the sweep => same sums. A record costs
+// one 8-byte store per block instead of one store sequence per survivor (~6
+// per block at the BASELINE decks), and the list is ~half the bytes.
 // AXIS = the fp32 pre-filter's per-axis test (axis_mode == 2).
 //
-// Predicated list store: address = lane base + c * 128 B in one wide multiply-add
-// (the compiler otherwise rebuilds the 64-bit address from the kernel parameter
-// for every candidate, ~10 instructions per store).
-__device__ __forceinline__ void st_list_if(uint32_t* base, unsigned c, uint32_t v, bool p) {
+// Record store: address = lane base + r * 256 B in one wide multiply-add (the
+// compiler otherwise rebuilds the 64-bit address from the kernel parameter).
+__device__ __forceinline__ void st_rec(uint2* base, unsigned r, uint32_t v, uint32_t m) {
     asm volatile(
-        "{\n\t.reg .pred q;\n\t.reg .u64 a;\n\t"
-        "setp.ne.u32 q, %3, 0;\n\t"
-        "mad.wide.u32 a, %1, 128, %0;\n\t"
-        "@q st.global.u32 [a], %2;\n\t}"
+        "{\n\t.reg .u64 a;\n\t"
+        "mad.wide.u32 a, %1, 256, %0;\n\t"
+        "st.global.v2.u32 [a], {%2, %3};\n\t}"
         :
-        : "l"(base), "r"(c), "r"(v), "r"((unsigned)p)
+        : "l"(base), "r"(r), "r"(v), "r"(m)
         : "memory");
+}
+
+// Emit one 32-candidate block's survivors (m != 0) as a record.
+__device__ __forceinline__ void emit_rec(uint2* rec, int cap, int& nrec, int& cnt, uint32_t v,
+                                         uint32_t m) {
+    if (m) {
+        if (nrec < cap) st_rec(rec, (unsigned)nrec, v, m);
+        ++nrec;
+        cnt += __popc(m);
+    }
 }
 
 template <int DIM, bool ORDERED, bool AXIS>
 __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict__ xl4, int k,
-                                          float pre_r, uint32_t* lst, int cap) {
+                                          float pre_r, uint2* lst, int cap, int& nrec) {
     const DomainDev& d = g.dom;
     int ci[3] = {0, 0, 0};
     decode_cell<DIM>(d, g.key[k], ci);
@@ -367,9 +380,7 @@ __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict
             return !(rej || r2 > r2lim);
         };
         // Blocks of 32 candidates: the tests set a bit mask (eight loads in flight,
-        // tail loads clamped and masked off), then the set bits are expanded
-        // into list entries - ~1/6 of the candidates, instead of a predicated
-        // store sequence for every candidate.
+        // tail loads clamped and masked off), stored as one record.
         for (int t = s; t < e; t += 32) {
             const int nb = min(32, e - t);
             uint32_t m = 0;
@@ -391,23 +402,7 @@ __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict
                 }
             }
             if (nb < 32) m &= (1u << nb) - 1u;
-            const uint32_t v = (uint32_t)t | icode;
-            if (cnt + __popc(m) <= cap) {
-                unsigned c = (unsigned)cnt;
-                while (m) {
-                    const int b = __ffs(m) - 1;
-                    m &= m - 1;
-                    st_list_if(lst, c++, v + b, true);
-                }
-                cnt = (int)c;
-            } else {
-                while (m) {
-                    const int b = __ffs(m) - 1;
-                    m &= m - 1;
-                    if (cnt < cap) lst[cnt * 32] = v + b;
-                    ++cnt;
-                }
-            }
+            emit_rec(lst, cap, nrec, cnt, (uint32_t)t | icode, m);
         }
     }
     return cnt;
@@ -416,13 +411,14 @@ __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict
 // Evaluate fn(j, rel, mask, payload) over a slot's list, payload = load(j) (the
 // pair's per-neighbour operands). Lane-private loop, software-pipelined: the
 // position / payload gathers run 2 pairs ahead of the arithmetic and the list
-// entries 4-5 pairs ahead, in three buffers with fixed roles (loop unrolled by
-// 3: no register rotation; profiles/r1_nl_*: the rotating version spent ~30
-// moves per pair and the one-ahead version stalled on long_scoreboard).
+// entries (expanded from the chunk records, the next record loaded one record
+// ahead) 4-5 pairs ahead, in buffers with fixed roles (loop unrolled: no
+// register rotation; profiles/r1_nl_*: the rotating version spent ~30 moves
+// per pair and the one-ahead version stalled on long_scoreboard).
 // AXIS = the exact fp64 per-axis test. FAST drops the reference's "+ 0.0" of the
 // direct image (it only normalises -0.0; FAST mode does not promise bitwise).
 template <int DIM, bool AXIS, bool FAST, int NB, class Load, class Fn>
-__device__ __forceinline__ void consume_list(const Geo& g, const uint32_t* __restrict__ lst, int cnt,
+__device__ __forceinline__ void consume_list(const Geo& g, const uint2* __restrict__ rec, int cnt,
                                              const double* xi, Load&& load, Fn&& fn) {
     constexpr uint32_t kM = (1u << kSlotBits) - 1;
     using P = decltype(load(0));
@@ -431,7 +427,20 @@ __device__ __forceinline__ void consume_list(const Geo& g, const uint32_t* __res
         double4 p;
         P pl;
     };
-    auto ent_at = [&](int s) { return s < cnt ? lst[s * 32] : 0u; };
+    // entry generator: entries are requested in increasing order, once each
+    uint2 cur = rec[0], nxt = rec[32];
+    int r = 0;
+    auto gen = [&]() -> uint32_t {
+        if (cur.y == 0) {
+            cur = nxt;
+            ++r;
+            nxt = rec[(r + 1) * 32];  // at most record `count`: the slack row
+        }
+        const uint32_t b = (uint32_t)(__ffs(cur.y) - 1);
+        cur.y &= cur.y - 1;
+        return cur.x + b;
+    };
+    auto nx = [&](int s) { return s < cnt ? gen() : 0u; };
     auto fetch = [&](Buf& b, uint32_t ent) {
         b.ent = ent;
         b.p = ld256(g.p4 + (ent & kM));
@@ -464,30 +473,32 @@ __device__ __forceinline__ void consume_list(const Geo& g, const uint32_t* __res
     };
     if constexpr (NB == 3) {
         Buf A, B, C;
-        uint32_t eA = ent_at(3), eB = ent_at(4), eC = ent_at(2);
-        fetch(A, ent_at(0));
-        fetch(B, ent_at(1));
+        const uint32_t e0 = nx(0), e1 = nx(1);
+        uint32_t eC = nx(2), eA = nx(3), eB = nx(4);
+        fetch(A, e0);
+        fetch(B, e1);
         for (int s = 0; s < cnt; s += 3) {
             fetch(C, eC);  // pair s + 2
-            eC = ent_at(s + 5);
+            eC = nx(s + 5);
             process(A);  // pair s
             fetch(A, eA);  // pair s + 3
-            eA = ent_at(s + 6);
+            eA = nx(s + 6);
             if (s + 1 < cnt) process(B);
             fetch(B, eB);  // pair s + 4
-            eB = ent_at(s + 7);
+            eB = nx(s + 7);
             if (s + 2 < cnt) process(C);
         }
     } else {  // two buffers: gathers one pair ahead (register-lean)
         Buf A, B;
-        uint32_t eA = ent_at(2), eB = ent_at(1);
-        fetch(A, ent_at(0));
+        const uint32_t e0 = nx(0);
+        uint32_t eB = nx(1), eA = nx(2);
+        fetch(A, e0);
         for (int s = 0; s < cnt; s += 2) {
             fetch(B, eB);  // pair s + 1
-            eB = ent_at(s + 3);
+            eB = nx(s + 3);
             process(A);  // pair s
             fetch(A, eA);  // pair s + 2
-            eA = ent_at(s + 4);
+            eA = nx(s + 4);
             if (s + 1 < cnt) process(B);
         }
     }
@@ -567,7 +578,7 @@ __device__ __forceinline__ float half_offset(const AxisOpts& ao, int ci, int o, 
 
 template <int DIM, bool ORDERED>
 __device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg, int k,
-                                               uint32_t* lst, int cap) {
+                                               uint2* lst, int cap, int& nrec) {
     const DomainDev& d = g.dom;
     const int flat_i = g.key[k];
     int ci[3] = {0, 0, 0};
@@ -657,34 +668,19 @@ __device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg,
                 }
             }
             if (o.ns - q0 < 32) m &= (1u << (o.ns - q0)) - 1u;
-            const uint32_t v = (uint32_t)(o.s + q0) | o.icode;
-            if (cnt + __popc(m) <= cap) {
-                unsigned c = (unsigned)cnt;
-                while (m) {
-                    const int b = __ffs(m) - 1;
-                    m &= m - 1;
-                    st_list_if(lst, c++, v + b, true);
-                }
-                cnt = (int)c;
-            } else {
-                while (m) {
-                    const int b = __ffs(m) - 1;
-                    m &= m - 1;
-                    if (cnt < cap) lst[cnt * 32] = v + b;
-                    ++cnt;
-                }
-            }
+            emit_rec(lst, cap, nrec, cnt, (uint32_t)(o.s + q0) | o.icode, m);
         }
     }
     return cnt;
 }
 
-struct NList {  // per-step neighbour lists (k_nlist in cells.cu)
-    const uint32_t* e;
-    const int* count;
-    int cap;
+struct NList {  // per-step neighbour lists (k_nlist in cells.cu): chunk records
+    const uint32_t* e;  // uint2 records (see st_rec), viewed as u32
+    const int* count;   // pairs (expanded entries) per slot
+    int cap;            // records per slot
 };
 
+// Record 0 of slot k, in uint2 units (record r is 32 r further).
 __device__ __forceinline__ size_t nlist_base(int k, int cap) {
     return (size_t)(k >> 5) * cap * 32 + (k & 31);
 }
@@ -702,7 +698,7 @@ __device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __rest
                                               Fn&& fn) {
     if constexpr (LIST) {
         if (!valid) return;
-        const uint32_t* lst = nl.e + nlist_base(k, nl.cap);
+        const uint2* lst = reinterpret_cast<const uint2*>(nl.e) + nlist_base(k, nl.cap);
         const int cnt = nl.count[k];
         const bool axis = FAST ? !(radius <= g.min_cs) : axis_mode(g, radius) != 0;
         if (!axis)
