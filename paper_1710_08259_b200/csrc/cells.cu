@@ -442,8 +442,8 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered) {
     const int b = blocks_for(n, T);
     const HalfGrid hg = half_grid(c, radius);
     for (int attempt = 0; attempt < 3; ++attempt) {
-        // uint2 records + one slack row (consume_list reads one record ahead)
-        const size_t need = slots * (size_t)c->nl_cap * 2 + 64;
+        // uint2 records + two slack rows (consume_list reads two records ahead)
+        const size_t need = slots * (size_t)c->nl_cap * 2 + 128;
         if (c->nl_len < need) {
             if (c->d_nlist) cudaFree(c->d_nlist);
             c->d_nlist = nullptr;

@@ -411,12 +411,16 @@ __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict
 // Evaluate fn(j, rel, mask, payload) over a slot's list, payload = load(j) (the
 // pair's per-neighbour operands). Lane-private loop, software-pipelined: the
 // position / payload gathers run 2 pairs ahead of the arithmetic and the list
-// entries (expanded from the chunk records, the next record loaded one record
-// ahead) 4-5 pairs ahead, in buffers with fixed roles (loop unrolled: no
+// entries (expanded from the chunk records, loaded two records ahead) 4-5 pairs ahead, in buffers with fixed roles (loop unrolled: no
 // register rotation; profiles/r1_nl_*: the rotating version spent ~30 moves
 // per pair and the one-ahead version stalled on long_scoreboard).
 // AXIS = the exact fp64 per-axis test. FAST drops the reference's "+ 0.0" of the
 // direct image (it only normalises -0.0; FAST mode does not promise bitwise).
+// NAU_GEN_SELECT: record switch by selects + a predicated load instead of a
+// divergent branch (measured: cfg1 -3%, cfg2 even)
+#ifndef NAU_GEN_SELECT
+#define NAU_GEN_SELECT 1
+#endif
 template <int DIM, bool AXIS, bool FAST, int NB, class Load, class Fn>
 __device__ __forceinline__ void consume_list(const Geo& g, const uint2* __restrict__ rec, int cnt,
                                              const double* xi, Load&& load, Fn&& fn) {
@@ -428,14 +432,26 @@ __device__ __forceinline__ void consume_list(const Geo& g, const uint2* __restri
         P pl;
     };
     // entry generator: entries are requested in increasing order, once each
-    uint2 cur = rec[0], nxt = rec[32];
+    // (records loaded two ahead: sparse records switch every 1-2 entries)
+    uint2 cur = rec[0], n1 = rec[32], n2 = rec[64];
     int r = 0;
     auto gen = [&]() -> uint32_t {
+#if NAU_GEN_SELECT
+        const bool sw = cur.y == 0;
+        cur.x = sw ? n1.x : cur.x;
+        cur.y = sw ? n1.y : cur.y;
+        n1.x = sw ? n2.x : n1.x;
+        n1.y = sw ? n2.y : n1.y;
+        r += sw;
+        if (sw) n2 = rec[(r + 2) * 32];
+#else
         if (cur.y == 0) {
-            cur = nxt;
+            cur = n1;
+            n1 = n2;
             ++r;
-            nxt = rec[(r + 1) * 32];  // at most record `count`: the slack row
+            n2 = rec[(r + 2) * 32];  // at most record `count` + 1: the slack rows
         }
+#endif
         const uint32_t b = (uint32_t)(__ffs(cur.y) - 1);
         cur.y &= cur.y - 1;
         return cur.x + b;

@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnau_b200.so")
+# NAU_LIB: an alternative build of the same library (tools/variants.sh experiments)
+LIB_PATH = os.environ.get("NAU_LIB") or os.path.join(HERE, "libnau_b200.so")
 
 PERIODIC, SYMMETRIC, CUTOFF = 0, 1, 2
 OPS = {"sph_S": 0, "sph_D00": 1, "sph_G11": 2, "sph_L0": 3, "sph_A": 4, "dem_l": 5,
