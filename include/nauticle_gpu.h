@@ -61,7 +61,8 @@ enum {
     NAU_OP_DEM_BOUNDARY = 6, /* dem_boundary_force         interactions.cpp:190-193 */
     NAU_OP_GRAVITY = 7,      /* nbody_gravity (m, G, eps)  interactions.cpp:195-214 */
     NAU_OP_DEM_LSD = 8,      /* dem_lsd (v,R,kn,en,m,cf,Rs) new: linear spring-dashpot + Coulomb */
-    NAU_OP_COUNT = 9
+    NAU_OP_SFM = 9,          /* sfm (v, v0, r_d, R, A, B, k, c, m, tau)  interactions.cpp:216-257 */
+    NAU_OP_COUNT = 10
 };
 
 /* Smoothing-kernel families: Wendland (keywords Wp5D220, src/kernel.cpp:9-69)

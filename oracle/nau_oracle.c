@@ -558,6 +558,43 @@ int nor_interact(int op, int kfamily, int kdim, nor_ps* ps, const nor_operand* o
             for (int c = 0; c < out_comps; ++c) out[(long)c * n + i] = acc[c];
             continue;
         }
+        if (op == NOR_SFM) { /* eval_social_force, interactions.cpp:216-257 */
+            double v_i[3], e0[3], drv[3] = {0, 0, 0};
+            for (int a = 0; a < d; ++a) v_i[a] = opv(&ops[0], n, a, i);
+            const double v0 = opv(&ops[1], n, 0, i);
+            const double radius_i = opv(&ops[3], n, 0, i);
+            const double rep_a = opv(&ops[4], n, 0, i), rep_b = opv(&ops[5], n, 0, i);
+            const double body_k = opv(&ops[6], n, 0, i), c_i = opv(&ops[7], n, 0, i);
+            const double m_i = opv(&ops[8], n, 0, i), tau = opv(&ops[9], n, 0, i);
+            if (!(tau > 0.0) || !(m_i > 0.0)) { /* 228-229 */
+                rc = 1;
+                *bad = i;
+                break;
+            }
+            for (int a = 0; a < d; ++a) e0[a] = opv(&ops[2], n, a, i) - ps->pos[(long)a * n + i];
+            const double e0n = norm_d(e0, d);
+            if (e0n > 0.0) {
+                const double s = v0 / e0n;
+                for (int a = 0; a < d; ++a) drv[a] = (e0[a] * s - v_i[a]) / tau;
+            } else {
+                ps->warnings++; /* agent already at its desired position */
+            }
+            double cs_min = ps->dom.cs[0];
+            for (int a = 1; a < d; ++a) cs_min = ps->dom.cs[a] < cs_min ? ps->dom.cs[a] : cs_min;
+            for (int k = 0; k < b.n; ++k) {
+                const cand_t* cd = &b.c[k];
+                const int j = cd->j;
+                const double d_ji = norm_d(cd->rel, d);
+                if (!(d_ji > 0.0 && d_ji < cs_min)) continue;
+                const double r_ij = radius_i + opv(&ops[3], n, 0, j);
+                const double c_ij = 0.5 * (c_i + opv(&ops[7], n, 0, j));
+                const double body = r_ij - d_ji > 0.0 ? body_k * (r_ij - d_ji) : 0.0;
+                const double s = rep_a * exp((r_ij - d_ji) / rep_b) + body - c_ij;
+                for (int a = 0; a < d; ++a) acc[a] = acc[a] + (cd->rel[a] / d_ji) * s;
+            }
+            for (int a = 0; a < d; ++a) out[(long)a * n + i] = drv[a] - acc[a] / m_i;
+            continue;
+        }
         /* DEM: dem_sum, interactions.cpp:152-193 (Hertz) / restated LSD law */
         {
             const int images_only = op == NOR_DEM_BOUNDARY;

@@ -26,7 +26,7 @@ enum { NOR_PERIODIC = 0, NOR_SYMMETRIC = 1, NOR_CUTOFF = 2 };
 /* Operator codes: same numbering as include/nauticle_gpu.h (NAU_OP_*). */
 enum {
     NOR_SPH_S = 0, NOR_SPH_D00 = 1, NOR_SPH_G11 = 2, NOR_SPH_L0 = 3, NOR_SPH_A = 4,
-    NOR_DEM_HERTZ = 5, NOR_DEM_BOUNDARY = 6, NOR_GRAVITY = 7, NOR_DEM_LSD = 8
+    NOR_DEM_HERTZ = 5, NOR_DEM_BOUNDARY = 6, NOR_GRAVITY = 7, NOR_DEM_LSD = 8, NOR_SFM = 9
 };
 enum { NOR_K_WENDLAND = 0, NOR_K_CUBIC = 1 };
 

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_build", "libnau_oracle.so")
 
 PERIODIC, SYMMETRIC, CUTOFF = 0, 1, 2
-SPH_S, SPH_D00, SPH_G11, SPH_L0, SPH_A, DEM_HERTZ, DEM_BOUNDARY, GRAVITY, DEM_LSD = range(9)
+SPH_S, SPH_D00, SPH_G11, SPH_L0, SPH_A, DEM_HERTZ, DEM_BOUNDARY, GRAVITY, DEM_LSD, SFM = range(10)
 K_WENDLAND, K_CUBIC = 0, 1
 
 

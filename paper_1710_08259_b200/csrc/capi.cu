@@ -42,6 +42,7 @@ const nau_op_info kOps[] = {
     {"dem_boundary_force", NAU_OP_DEM_BOUNDARY, 7, 7, -1, 6, 1},
     {"nbody_gravity", NAU_OP_GRAVITY, 2, 3, -1, -1, 0},
     {"dem_lsd", NAU_OP_DEM_LSD, 7, 7, -1, 6, 1},
+    {"sfm", NAU_OP_SFM, 10, 10, -1, -1, 1},
 };
 
 template <typename T>
@@ -174,6 +175,8 @@ const char* msg_text(int msg) {
         case nau::kMsgCoincident: return "nbody_gravity: coincident particles with zero softening";
         case nau::kMsgDemParams: return "dem contact: nonpositive Young modulus or radius";
         case nau::kMsgRandBounds: return "rand: lower bound exceeds upper bound";
+        case nau::kMsgSfmTau: return "sfm: relaxation time must be positive";
+        case nau::kMsgSfmMass: return "sfm: mass must be positive";
         default: return "runtime error";
     }
 }
@@ -755,7 +758,7 @@ nau_status nau_interact(nau_ctx* c, int op, int kf, int kdim, const nau_operand*
     if (!field_ok(c, out_field) || out_field == 0)
         return fail(c, NAU_ERR_ARG, "bad output field (r is written by euler only)");
     const int dim = c->dom.dim;
-    nau::Opd d_ops[8];
+    nau::Opd d_ops[10];
     for (int k = 0; k < nops; ++k) {
         if (ops[k].field_id >= 0 && !field_ok(c, ops[k].field_id))
             return fail(c, NAU_ERR_ARG, "bad operand field id");
@@ -773,7 +776,26 @@ nau_status nau_interact(nau_ctx* c, int op, int kf, int kdim, const nau_operand*
     int ar = 1, acl = 1;
     shape(0, ar, acl);
     int out_rows = 1, out_cols = 1;
-    if (op == NAU_OP_SPH_S) {
+    auto shape_str = [](int r, int cc) { return std::to_string(r) + "x" + std::to_string(cc); };
+    if (op == NAU_OP_SFM) {
+        // eval_social_force (interactions.cpp:216-257): r_d - x_i and (...) - v_i are
+        // d-vector differences, every other operand goes through .value()
+        out_rows = dim;
+        int r = 1, cc = 1;
+        for (int k : {1, 3, 4, 5, 6, 7, 8, 9}) {  // the scalar_operand calls, in order
+            shape(k, r, cc);
+            if (!(r == 1 && cc == 1))
+                return fail(c, NAU_ERR_RUNTIME,
+                            "expected a scalar, got a " + shape_str(r, cc) + " tensor");
+        }
+        shape(2, r, cc);
+        if (!(r == dim && cc == 1))
+            return fail(c, NAU_ERR_RUNTIME, "operator '-': incompatible shapes " +
+                                                shape_str(r, cc) + " and " + shape_str(dim, 1));
+        if (!(ar == dim && acl == 1))
+            return fail(c, NAU_ERR_RUNTIME, "operator '-': incompatible shapes " +
+                                                shape_str(dim, 1) + " and " + shape_str(ar, acl));
+    } else if (op == NAU_OP_SPH_S) {
         out_rows = ar;
         out_cols = acl;
     } else if (op == NAU_OP_SPH_D00 || op == NAU_OP_SPH_L0) {

@@ -9,6 +9,7 @@
 // This TU is compiled with -fmad=false: with IEEE div/sqrt the results are
 // bitwise identical to the reference wherever no libm transcendental (pow/log)
 // enters (Hertz DEM, gravity, Tait EOS are tolerance-checked).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -282,6 +283,78 @@ __global__ void __launch_bounds__(kThreads) k_dem(const __grid_constant__ DemArg
         if (!isfinite(r)) latch_error(a.err, 2, kMsgNan, my_orig);
         a.out[d * n + k] = r;
     }
+}
+
+// ---- social force model: eval_social_force (interactions.cpp:216-257) ----
+// Agents i: driving term (e0 * (v0/|e0|) - v_i) / tau toward r_d, minus the sum
+// over candidates 0 < d < min cell size of n_ji * (A exp((r_ij - d)/B) + body
+// - c_ij), divided by m_i. Operands 3 (radius) and 7 (c) are read at j; the
+// pair rule ignores mirror guides (the reference passes none to it).
+struct SfmArgs {
+    Geo g;
+    const float4* xl;
+    Opd v, v0, rd, rad, A, B, K, cc, m, tau;
+    double cs_min;
+    double* out;
+    DevErr* err;
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(kThreads) k_sfm(const __grid_constant__ SfmArgs a) {
+    const Geo& g = a.g;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    bool valid = k < *g.nact;
+    const int kk = valid ? k : 0;
+    const long n = g.n;
+    double xi[3] = {0.0, 0.0, 0.0}, v_i[3] = {0.0, 0.0, 0.0}, e0[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+        xi[d] = g.x[d * n + kk];
+        v_i[d] = a.v.at(d, kk, n);
+    }
+    const double v0 = a.v0.at(0, kk, n), radius_i = a.rad.at(0, kk, n);
+    const double rep_a = a.A.at(0, kk, n), rep_b = a.B.at(0, kk, n), body_k = a.K.at(0, kk, n);
+    const double c_i = a.cc.at(0, kk, n), m_i = a.m.at(0, kk, n), tau = a.tau.at(0, kk, n);
+    const int my_orig = g.orig[kk];
+    if (valid && !(tau > 0.0)) {
+        latch_error(a.err, 1, kMsgSfmTau, my_orig);
+        valid = false;
+    } else if (valid && !(m_i > 0.0)) {
+        latch_error(a.err, 1, kMsgSfmMass, my_orig);
+        valid = false;
+    }
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) e0[d] = a.rd.at(d, kk, n) - xi[d];
+    const double e0n = norm_rel<DIM>(e0);
+    double drv[3] = {0.0, 0.0, 0.0};
+    if (e0n > 0.0) {
+        const double s = v0 / e0n;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) drv[d] = (e0[d] * s - v_i[d]) / tau;
+    } else if (valid) {
+        atomicAdd(&a.err->warnings, 1ull);  // agent already at its desired position
+    }
+    const double cs_min = a.cs_min;
+    double acc[3] = {0.0, 0.0, 0.0};
+    sweep<DIM, true>(g, a.xl, k, valid, xi, cs_min, [&](int j, const double* rel, int) {
+        const double d_ji = norm_rel<DIM>(rel);
+        if (!(d_ji > 0.0 && d_ji < cs_min)) return;
+        const double r_ij = radius_i + a.rad.at(0, j, n);
+        const double c_ij = 0.5 * (c_i + a.cc.at(0, j, n));
+        const double body = r_ij - d_ji > 0.0 ? body_k * (r_ij - d_ji) : 0.0;
+        const double s = rep_a * exp((r_ij - d_ji) / rep_b) + body - c_ij;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) acc[d] = acc[d] + (rel[d] / d_ji) * s;
+    });
+    if (!valid) return;
+    bool bad = false;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+        const double r = drv[d] - acc[d] / m_i;
+        bad |= !isfinite(r);
+        a.out[d * n + k] = r;
+    }
+    if (bad) latch_error(a.err, 2, kMsgNan, my_orig);
 }
 
 // ---- all-pairs softened gravity: eval_gravity (interactions.cpp:195-214) ----
@@ -586,6 +659,31 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
             if (fast) k_gravity<3, true><<<blocks, kGravTile, 0, c->stream>>>(a);
             else k_gravity<3, false><<<blocks, kGravTile, 0, c->stream>>>(a);
         }
+        prof_end(c, 100 + op);
+    } else if (op == NAU_OP_SFM) {
+        SfmArgs a;
+        a.g = make_geo(c);
+        a.xl = c->d_xl;
+        a.v = ops[0];
+        a.v0 = ops[1];
+        a.rd = ops[2];
+        a.rad = ops[3];
+        a.A = ops[4];
+        a.B = ops[5];
+        a.K = ops[6];
+        a.cc = ops[7];
+        a.m = ops[8];
+        a.tau = ops[9];
+        double cs_min = c->dom.cs[0];  // interactions.cpp:239-240
+        for (int d = 1; d < dim; ++d) cs_min = std::min(cs_min, c->dom.cs[d]);
+        a.cs_min = cs_min;
+        a.out = out;
+        a.err = c->d_err;
+        const int blocks = (int)((c->n + kThreads - 1) / kThreads);
+        prof_begin(c, 100 + op);
+        if (dim == 1) k_sfm<1><<<blocks, kThreads, 0, c->stream>>>(a);
+        else if (dim == 2) k_sfm<2><<<blocks, kThreads, 0, c->stream>>>(a);
+        else k_sfm<3><<<blocks, kThreads, 0, c->stream>>>(a);
         prof_end(c, 100 + op);
     } else {
         DemArgs a;

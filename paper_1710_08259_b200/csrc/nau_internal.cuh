@@ -52,6 +52,8 @@ enum ErrMsg {
     kMsgDemParams = 5,
     kMsgNan = 6,
     kMsgRandBounds = 7,
+    kMsgSfmTau = 8,
+    kMsgSfmMass = 9,
 };
 
 // Operand as seen by a kernel: field pointer (cell order) or uniform value.

@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("NAU_LIB") or os.path.join(HERE, "libnau_b200.so")
 
 PERIODIC, SYMMETRIC, CUTOFF = 0, 1, 2
 OPS = {"sph_S": 0, "sph_D00": 1, "sph_G11": 2, "sph_L0": 3, "sph_A": 4, "dem_l": 5,
-       "dem_boundary_force": 6, "nbody_gravity": 7, "dem_lsd": 8}
+       "dem_boundary_force": 6, "nbody_gravity": 7, "dem_lsd": 8, "sfm": 9}
 K_WENDLAND, K_CUBIC = 0, 1
 MODE_EXACT, MODE_FAST = 0, 1
 STATUS = {0: "ok", 1: "runtime error", 2: "runtime NaN", 3: "CUDA error", 4: "argument error",

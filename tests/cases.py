@@ -32,7 +32,10 @@ def random_spec(rng, dim=None, n=None, kinds=None, cells=None, cs=0.3):
             "Rp": rng.uniform(0.05, 0.15, (1, n)),
         },
         "consts": {"m": 0.5, "R": R, "E": 2.06e6, "nu": 0.33, "kn": 1e5, "en": 0.5, "cf": 0.5,
-                   "cf0": 0.0, "G": 1.0, "eps": 0.01, "Rs": R},
+                   "cf0": 0.0, "G": 1.0, "eps": 0.01, "Rs": R,
+                   # sfm (social force) parameters: desired speed, repulsion A/B,
+                   # body stiffness, attraction c, relaxation time
+                   "sv0": 1.3, "sA": 2.0, "sB": 0.08, "sK": 120.0, "sC": 0.05, "stau": 0.5},
     }
 
 
@@ -57,6 +60,9 @@ def op_list(dim):
          port.DEM_BOUNDARY, 0),
         ("dem_lsd", ["V", "Rp", "kn", "en", "M", "cf", "Rs"], None, dim, port.DEM_LSD, 0),
         ("nbody_gravity", ["M", "G", "eps"], None, dim, port.GRAVITY, 0),
+        # r_d = V: the desired positions are any d-vector field
+        ("sfm", ["V", "sv0", "V", "Rp", "sA", "sB", "sK", "sC", "M", "stau"], None, dim,
+         port.SFM, 0),
     ]
     return out
 

@@ -50,7 +50,7 @@ def test_registry_mirrors_reference_kops(lib):
         "sph_G11": (5, 5, 3, 4, True), "sph_L0": (5, 5, 3, 4, True),
         "sph_A": (5, 5, 3, 4, True), "dem_l": (7, 7, -1, 6, True),
         "dem_boundary_force": (7, 7, -1, 6, True), "nbody_gravity": (2, 3, -1, -1, False),
-        "dem_lsd": (7, 7, -1, 6, True),
+        "dem_lsd": (7, 7, -1, 6, True), "sfm": (10, 10, -1, -1, True),
     }
     for name, (amin, amax, ks, rs, fin) in expect.items():
         info = nau.find_interaction(name)

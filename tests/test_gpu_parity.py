@@ -22,7 +22,7 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 TOL_STEP = 1e-10
 TOL_10 = 1e-6
-TRANSCENDENTAL = {"dem_l", "dem_boundary_force", "nbody_gravity"}
+TRANSCENDENTAL = {"dem_l", "dem_boundary_force", "nbody_gravity", "sfm"}  # libm pow/exp
 
 
 def rel_err(a, b):
@@ -153,6 +153,93 @@ def test_errors_surface_like_the_reference(ctx):
         ctx.sync()
     assert e.value.status == 2
     ctx.sync()  # error word cleared
+
+
+def _sfm_ctx(pos, vel, tau=0.5, v0=1.3):
+    """The reference's sfm KAT deck (test_interactions.cpp:408-420): 8 x 8 cut-off
+    cells of 1 m, A = 2000, B = 0.08, k = 1.2e5, R = 0.25, c = 0, m = 70."""
+    c = nau.Context(0)
+    c.set_domain(2, [0, 0], [8, 8], [1.0, 1.0], [nau.CUTOFF, nau.CUTOFF])
+    n = len(pos)
+    c.set_particles(np.array(pos, dtype=np.float64).T.copy())
+    c.add_field("v", 2, 1, np.array(vel, dtype=np.float64).T.copy())
+    c.add_field("rdes", 2, 1, np.tile([[1000.0], [4.0]], (1, n)))
+    c.add_field("a", 2, 1, 0.0)
+    return c, ["v", v0, "rdes", 0.25, 2000.0, 0.08, 1.2e5, 0.0, 70.0, tau]
+
+
+def test_sfm_reference_kats():
+    """test_interactions.cpp:408-445 through the C-ABI: a relaxed agent feels no
+    force, a resting one accelerates at v0/tau, an overlapping pair is symmetric
+    and matches the hand formula."""
+    v0, tau = 1.3, 0.5
+    c, ops = _sfm_ctx([(4, 4)], [(v0, 0)])
+    c.interact("sfm", ops, "a")
+    assert np.linalg.norm(c.download("a")[:, 0]) <= 1e-9
+    c.close()
+    c, ops = _sfm_ctx([(4, 4)], [(0, 0)])
+    c.interact("sfm", ops, "a")
+    a = c.download("a")[:, 0]
+    assert abs(a[0] - v0 / tau) <= 1e-6 * v0 / tau and abs(a[1]) <= 1e-5
+    c.close()
+    c, ops = _sfm_ctx([(4.0, 4.0), (4.3, 4.0)], [(0, 0), (0, 0)])
+    ops[1] = 0.0
+    c.interact("sfm", ops, "a")
+    a = c.download("a")
+    assert np.linalg.norm(a[:, 0] + a[:, 1]) <= 1e-12 * np.linalg.norm(a[:, 0])
+    d, rij = 0.3, 0.5
+    f = 2000.0 * np.exp((rij - d) / 0.08) + 1.2e5 * (rij - d)
+    assert abs(a[0, 0] - (-f / 70.0)) <= 1e-12 * f / 70.0
+    c.close()
+
+
+def test_sfm_errors_and_warnings(ctx):
+    """sfm's own checks (interactions.cpp:228-229; the lowest offending index),
+    the Tensor shape messages of its operand algebra, and one warning per agent
+    already at its desired position."""
+    rng = np.random.default_rng(4)
+    spec = cases.random_spec(rng, dim=2, n=200, kinds=[2, 2], cells=[3, 3])
+    cases.gpu_context(spec, ctx)
+    ctx.add_field("o2", 2, 1, 0.0)
+    base = ["V", 1.3, "V", "Rp", 2.0, 0.08, 120.0, 0.05, "M", 0.5]
+    for slot, msg in ((9, "relaxation time"), (8, "mass")):
+        bad = list(base)
+        bad[slot] = 0.0
+        ctx.interact("sfm", bad, "o2")
+        with pytest.raises(nau.NauError) as e:
+            ctx.sync()
+        assert e.value.status == 1 and f"sfm: {msg} must be positive" in e.value.message
+    m = spec["fields"]["M"].copy()
+    m[0, [37, 11, 90]] = -1.0
+    ctx.add_field("Mbad", 1, 1, m)
+    bad = list(base)
+    bad[8] = "Mbad"
+    ctx.interact("sfm", bad, "o2")
+    with pytest.raises(nau.NauError) as e:
+        ctx.sync()
+    assert e.value.particle == 11
+    for slot, text in ((2, "operator '-': incompatible shapes 1x1 and 2x1"),
+                       (0, "operator '-': incompatible shapes 2x1 and 1x1"),
+                       (4, "expected a scalar, got a 2x1 tensor")):
+        bad = list(base)
+        bad[slot] = "A" if slot != 4 else "V"
+        with pytest.raises(nau.NauError) as e:
+            ctx.interact("sfm", bad, "o2")
+        assert text in e.value.message, e.value.message
+    ctx.add_field("rhere", 2, 1, ctx.download("r"))
+    w0 = ctx.warning_count
+    at_goal = list(base)
+    at_goal[2] = "rhere"
+    ctx.interact("sfm", at_goal, "o2")
+    ctx.sync()
+    assert ctx.warning_count - w0 == 200
+    ps = cases.port_system(spec)
+    from oracle import port
+    ops = [cases.port_operand(spec, o) if isinstance(o, str) and o != "rhere" else o
+           for o in at_goal]
+    ops[2] = ps.pos
+    want = ps.interact(port.SFM, ops, (2, 1))
+    assert rel_err(ctx.download("o2"), want) <= TOL_STEP
 
 
 def test_microbench_golden(ctx):
