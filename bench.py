@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slab", action="store_true",
                     help="cfg0/cfg2: run the slab-decomposed path even on one GPU")
+    ap.add_argument("--comm", default="torch", choices=["torch", "native"],
+                    help="slab exchange driver: torch.distributed (slab.py) or the "
+                         "library's own NCCL layer (nau_migrate / nau_halo_exchange)")
     ap.add_argument("--mode", default="fast", choices=["fast", "exact"],
                     help="fast: warp-per-particle sums (1e-10 tolerance); exact: reference order, bitwise")
     return ap.parse_args()
@@ -529,9 +532,10 @@ class DamBreakSlab(DamBreak):
 
     FIELDS = ["rho", "p", "v", "vdot", "mask"]
 
-    def __init__(self, dim, dist):
+    def __init__(self, dim, dist, native=False):
         super().__init__(dim)
         self.dist = dist
+        self.native = native  # exchange through the library's own NCCL layer (comm.cu)
 
     def setup(self, ctx):
         import torch
@@ -568,6 +572,12 @@ class DamBreakSlab(DamBreak):
         dev = self.backend.device
         ex = slab.Exchanger(self.dist.pg, rank, world, periodic, dev)
         self.rank_drv = slab.SlabRank(self.backend, ex, self.bounds, ncx, periodic)
+        if self.native:
+            uid = [nau.Context.comm_unique_id() if rank == 0 else None]
+            if world > 1:
+                self.dist.pg.broadcast_object_list(uid, src=0)
+            ctx.comm_init(uid[0], world, rank)
+            ctx.slab_config(0, self.bounds, periodic, slab.SlabRank.GHOST_PLANES)
         self.n_active = int((rows[:, -1] == 0).sum())
         N = float(len(rows))
         self.kernels = {
@@ -585,7 +595,12 @@ class DamBreakSlab(DamBreak):
         self.d2h = self.h_rows.numel() * 8
 
     def step(self, ctx):
-        self.rank_drv.step()
+        if self.native:  # nau_wcsph_step; nau_migrate; nau_halo_exchange (comm.cu)
+            ctx.wcsph_step(self.p)
+            ctx.migrate()
+            ctx.halo_exchange()
+        else:
+            self.rank_drv.step()
 
     def e2e_step(self, ctx):
         import torch
@@ -603,6 +618,7 @@ class DamBreakSlab(DamBreak):
         c.pop("neighbours_per_particle", None)
         c["slabs"] = self.bounds
         c["ghost_planes"] = 2
+        c["exchange"] = "native NCCL (comm.cu)" if self.native else "torch.distributed (slab.py)"
         return c
 
 
@@ -667,9 +683,9 @@ class DemSlab(DemColumn):
                 "slabs": self.bounds, "ghost_planes": 2}
 
 
-def make_workload(cfg, dist=None, slab=False):
+def make_workload(cfg, dist=None, slab=False, native=False):
     if slab and cfg in (0, 2):
-        return DamBreakSlab(3 if cfg == 2 else 2, dist)
+        return DamBreakSlab(3 if cfg == 2 else 2, dist, native)
     if slab and cfg == 4:
         return GravityShard(dist)
     if slab and cfg == 3:
@@ -724,7 +740,7 @@ def run_ours(args, dist):
     from paper_1710_08259_b200 import nau
 
     use_slab = args.config in (0, 2, 3, 4) and (args.slab or dist.world > 1)
-    wl = make_workload(args.config, dist, use_slab)
+    wl = make_workload(args.config, dist, use_slab, args.comm == "native")
     ctx = nau.Context(dist.local)
     ctx.set_mode(args.mode == "fast")
     wl.setup(ctx)

@@ -306,6 +306,32 @@ nau_status nau_pack_rows(nau_ctx* ctx, const int* dev_slots, long m, double* dev
  * global index, so sums keep the single-GPU order. Marks cells dirty. */
 nau_status nau_load_rows(nau_ctx* ctx, const double* dev_rows, long m, int gid_field);
 
+/* ---- native slab exchange over NCCL (nau_comm_init /
+ * nau_halo_exchange / nau_migrate; comm.cu). One context per GPU and process;
+ * the caller ships the 128-byte id from rank 0 to the others (torch.distributed,
+ * MPI, a file). NCCL is bound at run time: NAU_ERR_COMM if absent. ---- */
+#define NAU_COMM_ID_BYTES 128
+nau_status nau_comm_unique_id(unsigned char* id_out /* NAU_COMM_ID_BYTES */);
+nau_status nau_comm_init(nau_ctx* ctx, const unsigned char* id, int nranks, int rank);
+void nau_comm_destroy(nau_ctx* ctx);
+/* Rank r owns cells [bounds[r], bounds[r+1]) along `axis` (bounds: nranks + 1
+ * cell-plane indices from 0 to the cell count) plus ghost copies of the
+ * `ghost_planes` planes beyond each face; gid_field / ghost_field are scalar
+ * fields holding the global index (the within-cell sort key) and the ghost flag. */
+nau_status nau_slab_config(nau_ctx* ctx, int axis, const int* bounds, int periodic,
+                           int ghost_planes, int gid_field, int ghost_field);
+/* Owned particles whose cell left the slab move to the owning neighbour; the
+ * context then holds its owned particles only. Syncs. */
+nau_status nau_migrate(nau_ctx* ctx);
+/* The first / last ghost_planes owned planes go to the neighbours; the context
+ * then holds owned + ghost particles (ghost flag 1). Syncs. */
+nau_status nau_halo_exchange(nau_ctx* ctx);
+/* The primitive under both: swap device row blocks (width doubles per row) with
+ * the left / right neighbours; received blocks stay valid until the next call. */
+nau_status nau_comm_swap(nau_ctx* ctx, const double* to_left, long n_left, const double* to_right,
+                         long n_right, int width, const double** from_left, long* nf_left,
+                         const double** from_right, long* nf_right);
+
 /* Surfaces latched device errors (≙ the exceptions above). */
 nau_status nau_sync(nau_ctx* ctx);
 /* Message of the last error and the lowest original particle index involved (-1 if none). */

@@ -341,6 +341,7 @@ void nau_destroy(nau_ctx* c) {
         cudaStreamSynchronize(c->s_d2h);
     }
     if (c->stream) cudaStreamSynchronize(c->stream);
+    nau_comm_destroy(c);
     io_release(c);
     free_particles(c);
     free_cells(c);

@@ -321,8 +321,13 @@ __device__ __forceinline__ double mirror_comp(double v, int c, int rows, int col
 }  // namespace nau
 
 // Host-side context (capi.cu owns it; kernels*.cu receive plain arguments).
+namespace nau {
+struct SlabComm;  // comm.cu: native NCCL slab exchange
+}
+
 struct nau_ctx {
     int device = 0;
+    nau::SlabComm* slab = nullptr;  // nau_comm_init (comm.cu)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool has_domain = false;

@@ -41,7 +41,8 @@ EXPORTS = [
     "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows", "nau_dem_step",
     "nau_leapfrog_step", "nau_pack_sources", "nau_gravity_sources", "nau_set_neighbor_lists",
     "nau_upload_async", "nau_download_async", "nau_io_fence", "nau_io_join", "nau_eval",
-    "nau_set_random_state", "nau_get_random_counters",
+    "nau_set_random_state", "nau_get_random_counters", "nau_comm_unique_id", "nau_comm_init",
+    "nau_comm_destroy", "nau_slab_config", "nau_migrate", "nau_halo_exchange", "nau_comm_swap",
 ]
 
 
@@ -158,6 +159,13 @@ def load():
         "nau_eval": (i, [vp, C.POINTER(VmInstr), i, i, i]),
         "nau_set_random_state": (i, [vp, C.c_ulonglong, vp]),
         "nau_get_random_counters": (i, [vp, vp]),
+        "nau_comm_unique_id": (i, [vp]),
+        "nau_comm_init": (i, [vp, vp, i, i]),
+        "nau_comm_destroy": (None, [vp]),
+        "nau_slab_config": (i, [vp, i, vp, i, i, i, i]),
+        "nau_migrate": (i, [vp]),
+        "nau_halo_exchange": (i, [vp]),
+        "nau_comm_swap": (i, [vp, vp, l, vp, l, i, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -217,6 +225,56 @@ class Context:
         self.n = 0
         self.dim = 0
         self.fields = {}
+
+    # ---- native slab exchange over NCCL (comm.cu) ----
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """128-byte NCCL id (rank 0); ship it to the other ranks."""
+        L = load()
+        buf = (C.c_ubyte * 128)()
+        if L.nau_comm_unique_id(buf) != 0:
+            raise NauError(5, "NCCL unavailable")
+        return bytes(buf)
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int):
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        self._check(self.L.nau_comm_init(self.h, buf, nranks, rank))
+
+    def slab_config(self, axis, bounds, periodic, ghost_planes=2, gid="gid", ghost="ghost"):
+        b = np.ascontiguousarray(bounds, dtype=np.int32)
+        self._check(self.L.nau_slab_config(self.h, axis, b.ctypes.data, int(periodic),
+                                           ghost_planes, self._fid(gid), self._fid(ghost)))
+
+    def migrate(self):
+        self._check(self.L.nau_migrate(self.h))
+        self.n = self.L.nau_particle_count(self.h)
+
+    def halo_exchange(self):
+        self._check(self.L.nau_halo_exchange(self.h))
+        self.n = self.L.nau_particle_count(self.h)
+
+    def comm_swap(self, to_left, to_right):
+        """Swap device row blocks (torch float64, rows x width) with the neighbours;
+        returns (from_left, from_right) as torch device tensors (copies)."""
+        import torch
+        w = int(to_left.shape[1])
+        fl, fr = C.c_void_p(), C.c_void_p()
+        nl, nr = C.c_long(), C.c_long()
+        self._check(self.L.nau_comm_swap(self.h, to_left.data_ptr(), to_left.shape[0],
+                                         to_right.data_ptr(), to_right.shape[0], w,
+                                         C.byref(fl), C.byref(nl), C.byref(fr), C.byref(nr)))
+        self.sync()
+        out = []
+        for p, m in ((fl, nl.value), (fr, nr.value)):
+            if m == 0:
+                out.append(torch.empty((0, w), dtype=torch.float64, device=to_left.device))
+                continue
+
+            class _View:  # the library-owned receive buffer as a CUDA array
+                __cuda_array_interface__ = {"shape": (m, w), "typestr": "<f8",
+                                            "data": (p.value, False), "version": 2}
+            out.append(torch.as_tensor(_View(), device=to_left.device).clone())
+        return out[0], out[1]
 
     def close(self):
         if getattr(self, "h", None):

@@ -708,6 +708,64 @@ def test_slab_path_single_rank_matches_plain(ctx):
     ctx2.close()
 
 
+def test_native_slab_exchange_single_rank_matches_plain(ctx):
+    """nau_comm_init / nau_migrate / nau_halo_exchange (comm.cu, NCCL bound at run
+    time) on one rank: the step loop through the native exchange = the plain path,
+    bitwise (same check as the torch.distributed driver above)."""
+    import bench
+
+    class D:
+        world, rank, local, pg = 1, 0, 0, None
+
+    sc_args = dict(dx=0.05, fluid=(1.0, 1.0), tank=(2.0, 1.6))
+    plain = bench.DamBreak(2)
+    plain.sc = scenes.dam_break(2, **sc_args)
+    plain.sc.fields["v"][0, : plain.sc.params["n_fluid"]] = 3.0
+    ctx.set_mode(False)
+    plain.setup(ctx)
+    for _ in range(8):
+        plain.step(ctx)
+    ref_r, ref_v = ctx.download("r"), ctx.download("v")
+    ctx2 = nau.Context(0)
+    sl = bench.DamBreakSlab(2, D(), native=True)
+    sl.sc = scenes.dam_break(2, **sc_args)
+    sl.sc.fields["v"][0, : sl.sc.params["n_fluid"]] = 3.0
+    sl.setup(ctx2)
+    for _ in range(8):
+        sl.step(ctx2)
+    gid = ctx2.download("gid")[0].astype(int)
+    r2, v2 = np.empty_like(ref_r), np.empty_like(ref_v)
+    r2[:, gid], v2[:, gid] = ctx2.download("r"), ctx2.download("v")
+    np.testing.assert_array_equal(r2, ref_r)
+    np.testing.assert_array_equal(v2, ref_v)
+    ctx2.close()
+
+
+def test_native_comm_swap_on_a_one_rank_ring():
+    """nau_comm_swap through real NCCL send/recv: on a 1-rank periodic ring both
+    neighbours are this rank, so (posting order, slab.py Exchanger.swap) the block
+    sent left comes back from the right and vice versa; empty blocks too."""
+    import torch
+    c = nau.Context(0)
+    try:
+        c.set_domain(1, [0], [4], [0.25], [nau.PERIODIC])
+        c.set_particles(np.array([[0.1, 0.4, 0.6, 0.9]]))
+        c.add_field("gid", 1, 1, np.arange(4.0))
+        c.add_field("ghost", 1, 1, 0.0)
+        c.comm_init(nau.Context.comm_unique_id(), 1, 0)
+        c.slab_config(0, [0, 4], True, 1)
+        a = torch.arange(21, dtype=torch.float64, device="cuda").reshape(7, 3)
+        b = -torch.arange(6, dtype=torch.float64, device="cuda").reshape(2, 3)
+        fl, fr = c.comm_swap(a, b)
+        assert torch.equal(fr, a) and torch.equal(fl, b)
+        fl, fr = c.comm_swap(b[:0], a)
+        assert fr.shape == (0, 3) and torch.equal(fl, a)
+        with pytest.raises(nau.NauError):  # bounds must cover the axis
+            c.slab_config(0, [0, 3], True, 1)
+    finally:
+        c.close()
+
+
 # ------------------------------------------------------------- DEM / n-body ----
 def _dem_port_step(ps, st, prm, R, m):
     """vdot = dem_lsd(v,R,kn,en,m,cf,Rs) + g; v = euler(v,vdot,dt); r = euler(r,v,dt); shift."""
