@@ -332,6 +332,44 @@ nau_status nau_comm_swap(nau_ctx* ctx, const double* to_left, long n_left, const
                          long n_right, int width, const double** from_left, long* nf_left,
                          const double** from_right, long* nf_right);
 
+/* ---- result frames and hot start (frames.cu) ----
+ * Legacy VTK PolyData exactly as the reference writes it (io/vtk.cpp:193-304):
+ * particles in original index order, scalars as SCALARS, d-vectors padded to 3
+ * as VECTORS, other shapes in FIELD PerParticle, big-endian doubles in BINARY
+ * files. The strings the host owns (the deck's equations, variables,
+ * constants, parameters) are passed as the reference formats them. */
+typedef struct {
+    int frame_index;
+    double time;
+    const char* domain_text;          /* NULL: built from the context (domain.cpp:68-83) */
+    const char* params_text;          /* "simulated_time=..." (vtk.cpp:204-206) */
+    int n_variables;
+    const char* const* variables;     /* "name=value" each (tensor.cpp:128-150) */
+    int n_constants;
+    const char* const* constants;
+    int n_equations;
+    const char* const* equations;     /* Equation::to_text() each */
+    int n_fields;                     /* workspace order, r excluded */
+    const int* field_ids;
+    const char* const* field_names;
+} nau_frame_meta;
+nau_status nau_write_vtk(nau_ctx* ctx, const char* path, int binary, const nau_frame_meta* meta);
+/* Reader (read_vtk, vtk.cpp:310-464): a host-side frame for a hot start. */
+typedef struct nau_vtk_frame nau_vtk_frame;
+nau_status nau_vtk_read(const char* path, nau_vtk_frame** out);
+void nau_vtk_free(nau_vtk_frame* frame);
+const char* nau_vtk_last_error(void);
+/* particle count; positions dim x n component-major, original order */
+long nau_vtk_points(const nau_vtk_frame* frame, int* dim, int* frame_index, double* time,
+                    const double** pos_soa);
+int nau_vtk_array_count(const nau_vtk_frame* frame);
+/* name of point array k; soa component-major [(col*rows + row)*n + i] */
+const char* nau_vtk_array(const nau_vtk_frame* frame, int k, int* rows, int* cols,
+                          const double** soa);
+/* CaseData string array `key` (domain, params, field_shapes, variables, constants, equations) */
+int nau_vtk_strings(const nau_vtk_frame* frame, const char* key, const char* const** items);
+long nau_vtk_rand_counters(const nau_vtk_frame* frame, const unsigned long long** counters);
+
 /* Surfaces latched device errors (≙ the exceptions above). */
 nau_status nau_sync(nau_ctx* ctx);
 /* Message of the last error and the lowest original particle index involved (-1 if none). */

@@ -38,6 +38,7 @@ def lib():
         L.nref_get_field.argtypes = [vp, cp, vp, C.POINTER(i), C.POINTER(i)]
         L.nref_add_equation.argtypes = [vp, cp, cp]
         L.nref_solve_step.argtypes = [vp, i]
+        L.nref_write_vtk.argtypes = [vp, cp, i, i, d, d]
         L.nref_eval.argtypes = [vp, cp, i, i, i, vp, C.POINTER(i)]
         L.nref_eval_law.argtypes = [vp, cp, i, C.POINTER(cp), i, i, i, i, vp, C.POINTER(i)]
         L.nref_boundary_shift.argtypes = [vp]
@@ -135,6 +136,11 @@ class RefCase:
     def equation(self, name, text):
         _check(lib().nref_add_equation(self.h, name.encode(), text.encode()))
         return self
+
+    def write_vtk(self, path, binary, frame_index=0, time=0.0, simulated_time=0.0):
+        """The reference's make_frame + write_vtk (io/vtk.cpp:193-304)."""
+        _check(lib().nref_write_vtk(self.h, str(path).encode(), int(binary), int(frame_index),
+                                    float(time), float(simulated_time)))
 
     def solve_step(self, threads=1):
         _check(lib().nref_solve_step(self.h, threads))

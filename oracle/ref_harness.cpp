@@ -44,6 +44,7 @@
 #include "nauticle/case.hpp"
 #include "nauticle/error.hpp"
 #include "nauticle/interactions.hpp"
+#include "nauticle/io/vtk.hpp"
 #include "nauticle/kernel.hpp"
 #include "nauticle/sfl/parser.hpp"
 
@@ -349,6 +350,18 @@ int nref_add_equation(void* p, const char* name, const char* text) {
         e.rhs = parse(h, t.substr(eq + 1));
         e.rhs->collect(e.info);
         h->cs->equations.push_back(std::move(e));
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+// The reference's result frame writer (io/vtk.cpp:193-304): make_frame + write_vtk.
+int nref_write_vtk(void* p, const char* path, int binary, int frame_index, double time,
+                   double simulated_time) {
+    try {
+        Ref* h = static_cast<Ref*>(p);
+        h->cs->parameters.simulated_time = simulated_time;
+        write_vtk(make_frame(*h->cs, frame_index, time), path,
+                  binary ? VtkFormat::Binary : VtkFormat::Ascii);
         return 0;
     } catch (const std::exception& e) { return fail(e); }
 }

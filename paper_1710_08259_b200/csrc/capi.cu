@@ -402,6 +402,8 @@ nau_status nau_set_domain(nau_ctx* c, int dim, const int* min_cells, const int* 
             if (k < 0 || k > 2) return fail(c, NAU_ERR_ARG, "unknown boundary kind");
         }
         d.cells[a] = mx - mn;
+        c->min_cells[a] = mn;
+        c->max_cells[a] = mx;
         d.cs[a] = cs;
         d.lo[a] = mn * cs;  // domain.hpp:28-30: products, not sums
         d.hi[a] = mx * cs;

@@ -328,6 +328,7 @@ struct SlabComm;  // comm.cu: native NCCL slab exchange
 struct nau_ctx {
     int device = 0;
     nau::SlabComm* slab = nullptr;  // nau_comm_init (comm.cu)
+    int min_cells[3] = {0, 0, 0}, max_cells[3] = {1, 1, 1};  // as given (frames.cu describe)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool has_domain = false;

@@ -43,6 +43,8 @@ EXPORTS = [
     "nau_upload_async", "nau_download_async", "nau_io_fence", "nau_io_join", "nau_eval",
     "nau_set_random_state", "nau_get_random_counters", "nau_comm_unique_id", "nau_comm_init",
     "nau_comm_destroy", "nau_slab_config", "nau_migrate", "nau_halo_exchange", "nau_comm_swap",
+    "nau_write_vtk", "nau_vtk_read", "nau_vtk_free", "nau_vtk_last_error", "nau_vtk_points",
+    "nau_vtk_array_count", "nau_vtk_array", "nau_vtk_strings", "nau_vtk_rand_counters",
 ]
 
 
@@ -166,6 +168,15 @@ def load():
         "nau_migrate": (i, [vp]),
         "nau_halo_exchange": (i, [vp]),
         "nau_comm_swap": (i, [vp, vp, l, vp, l, i, vp, vp, vp, vp]),
+        "nau_write_vtk": (i, [vp, C.c_char_p, i, vp]),
+        "nau_vtk_read": (i, [C.c_char_p, vp]),
+        "nau_vtk_free": (None, [vp]),
+        "nau_vtk_last_error": (C.c_char_p, []),
+        "nau_vtk_points": (l, [vp, vp, vp, vp, vp]),
+        "nau_vtk_array_count": (i, [vp]),
+        "nau_vtk_array": (C.c_char_p, [vp, i, vp, vp, vp]),
+        "nau_vtk_strings": (i, [vp, C.c_char_p, vp]),
+        "nau_vtk_rand_counters": (l, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -177,6 +188,54 @@ def load():
 
 def _p(a):
     return a.ctypes.data_as(C.c_void_p)
+
+
+class FrameMeta(C.Structure):
+    _fields_ = [("frame_index", C.c_int), ("time", C.c_double), ("domain_text", C.c_char_p),
+                ("params_text", C.c_char_p), ("n_variables", C.c_int),
+                ("variables", C.POINTER(C.c_char_p)), ("n_constants", C.c_int),
+                ("constants", C.POINTER(C.c_char_p)), ("n_equations", C.c_int),
+                ("equations", C.POINTER(C.c_char_p)), ("n_fields", C.c_int),
+                ("field_ids", C.POINTER(C.c_int)), ("field_names", C.POINTER(C.c_char_p))]
+
+
+def _strs(items):
+    arr = (C.c_char_p * max(1, len(items)))(*[s.encode() for s in items])
+    return len(items), arr
+
+
+def read_vtk(path):
+    """The reference's read_vtk (io/vtk.cpp:310-464) through the library: a dict with
+    dim, frame, time, pos (dim x n), arrays {name: (rows, cols) SoA}, strings, rand_counters."""
+    L = load()
+    h = C.c_void_p()
+    if L.nau_vtk_read(str(path).encode(), C.byref(h)) != 0:
+        raise NauError(1, L.nau_vtk_last_error().decode())
+    try:
+        dim, fidx, t, pp = C.c_int(), C.c_int(), C.c_double(), C.POINTER(C.c_double)()
+        n = L.nau_vtk_points(h, C.byref(dim), C.byref(fidx), C.byref(t), C.byref(pp))
+        pos = np.ctypeslib.as_array(pp, (dim.value * n,)).reshape(dim.value, n).copy() if n else \
+            np.zeros((dim.value, 0))
+        arrays = {}
+        for k in range(L.nau_vtk_array_count(h)):
+            r, cc, sp = C.c_int(), C.c_int(), C.POINTER(C.c_double)()
+            name = L.nau_vtk_array(h, k, C.byref(r), C.byref(cc), C.byref(sp)).decode()
+            comps = r.value * cc.value
+            arrays[name] = ((r.value, cc.value),
+                            np.ctypeslib.as_array(sp, (comps * n,)).reshape(comps, n).copy())
+        strings = {}
+        for key in ("domain", "params", "field_shapes", "variables", "constants", "equations"):
+            items = C.POINTER(C.c_char_p)()
+            m = L.nau_vtk_strings(h, key.encode(), C.byref(items))
+            if m:
+                strings[key] = [items[q].decode() for q in range(m)]
+        cp = C.POINTER(C.c_ulonglong)()
+        m = L.nau_vtk_rand_counters(h, C.byref(cp))
+        rc = np.ctypeslib.as_array(cp, (m,)).copy() if m else np.zeros(0, np.uint64)
+        return {"dim": dim.value, "frame": fidx.value, "time": t.value, "pos": pos,
+                "arrays": arrays, "strings": strings, "rand_counters": rc}
+    finally:
+        L.nau_vtk_free(h)
 
 
 def find_interaction(name):
@@ -387,6 +446,26 @@ class Context:
             for q, v in enumerate(ins["imm"]):
                 arr[k].imm[q] = v
         self._check(self.L.nau_eval(self.h, arr, len(program), result, self._fid(out)))
+
+    def write_vtk(self, path, binary, fields, frame_index=0, time=0.0, params_text=None,
+                  variables=(), constants=(), equations=(), domain_text=None):
+        """Result frame of the device state (nau_write_vtk; io/vtk.cpp:219-304 layout).
+        fields: names in workspace order (r excluded)."""
+        m = FrameMeta()
+        m.frame_index, m.time = int(frame_index), float(time)
+        m.domain_text = domain_text.encode() if domain_text else None
+        m.params_text = params_text.encode() if params_text else None
+        keep = []
+        for attr, items in (("variables", variables), ("constants", constants),
+                            ("equations", equations)):
+            cnt, arr = _strs(list(items))
+            keep.append(arr)
+            setattr(m, "n_" + attr, cnt)
+            setattr(m, attr, arr)
+        ids = (C.c_int * max(1, len(fields)))(*[self._fid(f) for f in fields])
+        cnt, names = _strs([f if isinstance(f, str) else f.name for f in fields])
+        m.n_fields, m.field_ids, m.field_names = cnt, ids, names
+        self._check(self.L.nau_write_vtk(self.h, str(path).encode(), int(binary), C.byref(m)))
 
     def set_random_state(self, seed, counters=None):
         """≙ the case's RandomState: seed + per-particle draw counters (original order)."""
