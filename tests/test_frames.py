@@ -97,3 +97,50 @@ def test_hot_start_round_trip(tmp_path):
         assert out.read_bytes() == open(gold, "rb").read()
     finally:
         c.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fast", [False, True])
+def test_split_run_equals_straight_run(tmp_path, fast):
+    """3D dam break: 6 steps straight = 3 steps, a BINARY frame, a hot start in a
+    fresh context from that frame, 3 more steps — bitwise (the frame restores the
+    whole state in original order, so the cell lists and sums are the same)."""
+    import test_gpu_parity as tg
+    from paper_1710_08259_b200 import scenes
+    sc = scenes.dam_break(3, dx=0.02)
+    names = ["rho", "p", "v", "vdot", "mask"]
+    a = nau.Context(0)
+    b = nau.Context(0)
+    try:
+        pa = tg._gpu_dam(a, sc)
+        a.set_mode(fast)
+        for _ in range(6):
+            a.wcsph_step(pa)
+        straight = {k: a.download(k) for k in ["r"] + names}
+        pb = tg._gpu_dam(b, sc)
+        b.set_mode(fast)
+        for _ in range(3):
+            b.wcsph_step(pb)
+        path = tmp_path / "split.vtk"
+        b.write_vtk(path, True, names, frame_index=3, time=3 * sc.params["dt"])
+        b.close()
+        f = nau.read_vtk(path)
+        b = nau.Context(0)
+        b.set_domain(sc.dim, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+        b.set_particles(f["pos"])
+        for k in names:
+            (r, cc), soa = f["arrays"][k]
+            b.add_field(k, r, cc, soa)
+        b.boundary_shift()
+        f_ids = b.fields
+        pb.f_rho, pb.f_p, pb.f_v, pb.f_vdot, pb.f_mask = (f_ids["rho"].id, f_ids["p"].id,
+                                                          f_ids["v"].id, f_ids["vdot"].id,
+                                                          f_ids["mask"].id)
+        b.set_mode(fast)
+        for _ in range(3):
+            b.wcsph_step(pb)
+        for k in ["r"] + names:
+            np.testing.assert_array_equal(b.download(k), straight[k], err_msg=k)
+    finally:
+        a.close()
+        b.close()
