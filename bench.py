@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Benchmark: particle-updates/s of the Nauticle hot path on B200 (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|1|0] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 0-4] [--impl ours|reference]
+                  [--mode fast|exact] [--slab] [--comm torch|native]
 
 Workloads (scenes.py; synthetic, seeded — no dataset exists for this path):
   --config 2  (default) BASELINE cfg2: 3D WCSPH dam break, 4.0 M fluid + 1.92 M wall
@@ -20,8 +21,11 @@ results copied back inside the timed region.
 --impl reference times the reference's own CPU implementation (oracle/_ref: the
 unmodified reference sources built on the shims) through its public API with
 all host threads, on a bounded sample of the same workload; rank 0 only.
-Multi-GPU (torchrun): every rank runs an independent replica of the workload
-(weak scaling, no data-path collective) — slab decomposition is future work.
+Multi-GPU (torchrun): cfg0/2/3 are slab-decomposed along x (whole cell planes per
+rank, two ghost planes per face, migration + ghost refresh over NCCL every step;
+--comm torch: slab.py over torch.distributed, --comm native: the library's own
+nau_migrate / nau_halo_exchange), cfg4 shards the bodies with an all-gather of the
+sources every step; `scaling` is "strong" (the workload is fixed as N grows).
 """
 from __future__ import annotations
 
