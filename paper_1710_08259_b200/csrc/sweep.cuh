@@ -421,7 +421,7 @@ __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict
 #ifndef NAU_GEN_SELECT
 #define NAU_GEN_SELECT 1
 #endif
-template <int DIM, bool AXIS, bool FAST, int NB, class Load, class Fn>
+template <int DIM, bool AXIS, bool FAST, int NB, bool IMG = true, class Load, class Fn>
 __device__ __forceinline__ void consume_list(const Geo& g, const uint2* __restrict__ rec, int cnt,
                                              const double* xi, Load&& load, Fn&& fn) {
     constexpr uint32_t kM = (1u << kSlotBits) - 1;
@@ -469,7 +469,7 @@ __device__ __forceinline__ void consume_list(const Geo& g, const uint2* __restri
         double rel[3] = {0.0, 0.0, 0.0};
         bool ok = true;
         int mask = 0;
-        if (c == 0) {
+        if (!IMG || c == 0) {  // !IMG: no periodic / symmetric axis, every code is 0
 #pragma unroll
             for (int a = 0; a < DIM; ++a) {
                 rel[a] = FAST ? xj[a] - xi[a] : (xj[a] + 0.0) - xi[a];
@@ -707,7 +707,10 @@ __device__ __forceinline__ size_t nlist_base(int k, int cap) {
 // radius): the per-axis test is skipped whenever radius <= every cell size —
 // a pair it would reject has |rel| > cell size >= radius up to one rounding,
 // i.e. q = 2 where W and dW/dq are zero.
-template <int DIM, bool ORDERED, bool LIST, bool FAST = false, int NB = 3, class Load, class Fn>
+// IMG = false: the domain has no periodic or symmetric axis (host-checked), so
+// every list entry is a direct image and the image branch compiles away.
+template <int DIM, bool ORDERED, bool LIST, bool FAST = false, int NB = 3, bool IMG = true,
+          class Load, class Fn>
 __device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __restrict__ xl4,
                                               const NList& nl, int k, bool valid,
                                               const double* xi, double radius, Load&& load,
@@ -718,9 +721,9 @@ __device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __rest
         const int cnt = nl.count[k];
         const bool axis = FAST ? !(radius <= g.min_cs) : axis_mode(g, radius) != 0;
         if (!axis)
-            consume_list<DIM, false, FAST, NB>(g, lst, cnt, xi, load, fn);
+            consume_list<DIM, false, FAST, NB, IMG>(g, lst, cnt, xi, load, fn);
         else
-            consume_list<DIM, true, FAST, NB>(g, lst, cnt, xi, load, fn);
+            consume_list<DIM, true, FAST, NB, IMG>(g, lst, cnt, xi, load, fn);
     } else {
         sweep<DIM, ORDERED>(g, xl4, k, valid, xi, radius,
                             [&](int j, const double* rel, int mask) { fn(j, rel, mask, load(j)); });
