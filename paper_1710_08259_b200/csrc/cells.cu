@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_nlist(const __grid_constant__
 // scatter per slot; the last slot of each cell writes its cell's +inf pads.
 __global__ void k_pcount(int nc, const int* count, int* pcount) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c <= nc) pcount[c] = c < nc ? (count[c] + 7) & ~7 : 0;
+    if (c <= nc) pcount[c] = c < nc ? (count[c] + 31) & ~31 : 0;
 }
 
 __global__ void k_half_coords(DomainDev d, long n, const double* pos, const int* key,
@@ -260,7 +260,9 @@ __global__ void k_half_coords(DomainDev d, long n, const double* pos, const int*
     const int c = key[k];
     if (c >= d.ncells) return;  // inactive tail
     const long rank = k - cell_start[c];
-    const long p = pstart[c] + rank;
+    // 32-slot blocks, halves interleaved (sweep.cuh HalfGrid): rank -> word rank % 16
+    auto at = [&](long r) { return pstart[c] + (r & ~31L) + 2 * (r & 15) + ((r >> 4) & 1); };
+    const long p = at(rank);
     int rem = c;
     bool esc = false;
     for (int a = 0; a < d.dim; ++a) {
@@ -275,9 +277,9 @@ __global__ void k_half_coords(DomainDev d, long n, const double* pos, const int*
     if (esc) atomicOr(escaped, 1);
     if (rank == cell_count[c] - 1) {
         const __half inf = __ushort_as_half((unsigned short)0x7c00);
-        const long pe = pstart[c] + ((cell_count[c] + 7) & ~7);
-        for (long q = p + 1; q < pe; ++q)
-            for (int a = 0; a < d.dim; ++a) h[a * hlen + q] = inf;
+        const long re = (cell_count[c] + 31) & ~31;
+        for (long r = rank + 1; r < re; ++r)
+            for (int a = 0; a < d.dim; ++a) h[a * hlen + at(r)] = inf;
     }
 }
 
@@ -378,8 +380,8 @@ static HalfGrid half_grid(nau_ctx* c, double radius) {
     for (int a = 1; a < d.dim; ++a) iso &= d.cs[a] == d.cs[0];
     const double rho = radius / d.cs[0];
     if (!iso || !(rho <= 1.5) || c->n == 0) return hg;
-    // padded cells plus 32 halves of slack (build_list_half reads whole 32-blocks)
-    const long hlen = ((c->n + 8L * (nc + 1) + 32) + 7) & ~7L;
+    // cells padded to 32-slot blocks (only non-empty cells pad) plus slack
+    const long hlen = ((c->n + 32L * std::min<long>(nc, c->n) + 64) + 7) & ~7L;
     if (c->hq_len < hlen) {
         if (c->d_hq) cudaFree(c->d_hq);
         c->d_hq = nullptr;

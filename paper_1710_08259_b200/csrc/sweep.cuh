@@ -547,15 +547,21 @@ __device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ x
 // Isotropic cells, radius <= 1.5 cell sizes, every particle inside its cell's
 // box (else the fp32 build_list runs). Each particle's coordinates relative to
 // its cell origin, in cell units, are stored as fp16 in a cell-padded layout
-// (every cell's range starts at a multiple of 8, pads = +inf), so one 128-bit
-// load brings 8 candidates per axis and HFMA2 tests two candidates per
+// (every cell's range starts at a multiple of 32, pads = +inf), so four 128-bit
+// loads bring a 32-candidate block per axis and HFMA2 tests two candidates per
 // instruction: rel_a = sg * h_j + (off_a - h_i), off_a = the option's cell offset
 // (-1, 0, 1; mirror-low 0 with sg = -1; mirror-high 2 with sg = -1).
+// Within a block the halves are INTERLEAVED: half2 word k holds candidates k and
+// k + 16, so d = r2 - lim has its two sign bits at 15 and 31 and
+// (d & 0x80008000) >> (15 - k) drops them on mask bits k and k + 16 — two integer
+// instructions per word instead of a compare-and-pack sequence.
 // Error bound (cell units): |h| < 1 rounds to 2^-12, off - h_i (|.| <= 2) to
 // 2^-11, the HFMA2 result (|rel| <= 2 near the threshold) to 2^-11: |rel error|
 // <= 1.25 * 2^-10; |rel| <= rho => sqrt(r2) <= rho + 0.0022 before the three
-// r2 roundings (<= 2^-10 each for r2 < 4): r2 <= (rho + 0.0022)^2 + 0.003 =: lim,
-// rounded up to fp16. A superset filter again; the fp64 test decides.
+// roundings of d = ((rx^2 - lim) + ry^2) + rz^2 (|d| < 4: <= 2^-10 each):
+// lim = (rho + 0.0022)^2 + 0.003, rounded up to fp16, makes d < 0 for every
+// candidate within rho. A superset filter again; the fp64 test decides. Pads
+// (+inf) give d = +inf: never set.
 struct HalfGrid {
     const __half* h[3];  // padded per-axis coordinates
     const int* pstart;   // padded start of each cell (multiple of 8)
@@ -604,12 +610,13 @@ __device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg,
     for (int a = 0; a < 3; ++a) ao[a] = AxisOpts{0, 1, 1};
 #pragma unroll
     for (int a = 0; a < DIM; ++a) ao[a] = axis_opts(d, a, ci[a]);
-    const int pk = hg.pstart[flat_i] + (k - g.cell_start[flat_i]);
+    const int rk = k - g.cell_start[flat_i];  // rank in the cell -> interleaved position
+    const int pk = hg.pstart[flat_i] + (rk & ~31) + 2 * (rk & 15) + ((rk >> 4) & 1);
     float hi[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int a = 0; a < DIM; ++a) hi[a] = __half2float(hg.h[a][pk]);
     const float rl = hg.rho + 0.0022f;
-    const __half2 lim2 = __half2half2(__float2half_ru(fmaf(rl, rl, 0.003f)));
+    const __half2 nlim2 = __hneg2(__half2half2(__float2half_ru(fmaf(rl, rl, 0.003f))));
     const int n01 = ao[0].cnt * (DIM > 1 ? ao[1].cnt : 1);
     const int ncombo = n01 * (DIM > 2 ? ao[2].cnt : 1);
     // option setup; the next option's cell-table reads are issued one option
@@ -662,15 +669,15 @@ __device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg,
                 const uint32_t* w[3] = {&hv[u][0].x, &hv[u][1].x, &hv[u][2].x};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    __half2 r2;
+                    __half2 dd = nlim2;
 #pragma unroll
                     for (int a = 0; a < DIM; ++a) {
                         const __half2 x2 = *reinterpret_cast<const __half2*>(w[a] + q);
                         const __half2 r = __hfma2(o.sg2[a], x2, o.bq2[a]);
-                        r2 = a == 0 ? __hmul2(r, r) : __hfma2(r, r, r2);
+                        dd = __hfma2(r, r, dd);
                     }
-                    const unsigned mk = __hle2_mask(r2, lim2);
-                    m |= ((mk & 1u) | ((mk >> 15) & 2u)) << (8 * u + 2 * q);
+                    const int kw = 4 * u + q;  // word kw: candidates kw, kw + 16
+                    m += (*reinterpret_cast<const uint32_t*>(&dd) & 0x80008000u) >> (15 - kw);
                 }
             }
             if (q0 == 0 && idx + 1 < ncombo) {
