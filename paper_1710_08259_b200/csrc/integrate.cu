@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_consta
     const double pr_i = p_i / (rho_i * rho_i);
     double G[3] = {0.0, 0.0, 0.0}, A[3] = {0.0, 0.0, 0.0};
     // per-neighbour operands (v_j, p_j / rho_j^2), gathered ahead of the pair arithmetic
-    auto load = [&](int j) { return ld256(a.vp + j); };
+    const Ld256 load{a.vp};
     for_neighbors<DIM, true, LIST, false, 2>(g, a.xl, a.nl, k, valid, xi, radius, load,
                [&](int j, const double* rel, int mask, const double4& pj) {
         const double dist = norm_rel<DIM>(rel);

@@ -524,6 +524,11 @@ struct NoPayload {};
 struct NoLoad {
     __device__ __forceinline__ NoPayload operator()(int) const { return NoPayload{}; }
 };
+// Per-neighbour 32-byte payload (e.g. the WCSPH momentum pass's (v, p/rho^2)).
+struct Ld256 {
+    const double4* p;
+    __device__ __forceinline__ double4 operator()(int j) const { return ld256(p + j); }
+};
 
 // Entry point: `radius` is the lane's acceptance radius (fp64); the per-axis
 // mode is the warp's maximum of axis_mode (BASELINE decks: radius = cell size,
