@@ -101,7 +101,9 @@ int nau_get_mode(nau_ctx* ctx);
 /* Neighbour lists (default on): the candidate scan runs once per cell build and
  * every SPH operator with a uniform radius (nau_interact, nau_wcsph_step) reads
  * the list; same candidates in the same order, so results are identical either
- * way. Off = each pass sweeps the cells itself. */
+ * way. on = 0: each pass sweeps the cells itself; 1: lists (paired lists for the
+ * FAST-mode Wendland nau_wcsph_step: one thread per two particles, shared
+ * gathers); 2: lists, per-particle only. */
 nau_status nau_set_neighbor_lists(nau_ctx* ctx, int on);
 /* Use an external CUDA stream (cudaStream_t), e.g. torch's current stream. NULL = own stream. */
 nau_status nau_set_stream(nau_ctx* ctx, void* stream);

@@ -884,13 +884,18 @@ nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
         if (s != NAU_OK) return s;
     }
     // Both passes of the step share one neighbour list (same candidates, same order).
-    const bool lists = nau::nlist_for(c, p->radius, c->mode == NAU_MODE_EXACT);
+    // FAST + Wendland + radius within a cell (no per-axis test): paired lists
+    double min_cs = c->dom.cs[0];
+    for (int a = 1; a < c->dom.dim; ++a) min_cs = std::min(min_cs, c->dom.cs[a]);
+    const bool pairs = c->mode == NAU_MODE_FAST && p->kernel_family == NAU_K_WENDLAND &&
+                       p->radius <= min_cs;
+    const int lists = nau::nlist_for(c, p->radius, c->mode == NAU_MODE_EXACT, pairs);
     if (c->mode == NAU_MODE_FAST) {
         nau::launch_wcsph_fast(c, p, c->d_aux, lists);
         nau::launch_symplectic(c, c->fields[p->f_v].d, c->fields[p->f_vdot].d,
                                p->f_mask >= 0 ? c->fields[p->f_mask].d : nullptr, p->dt);
     } else {
-        nau::launch_wcsph(c, p, lists);
+        nau::launch_wcsph(c, p, lists != 0);
     }
     c->dirty = true;
     return NAU_OK;
@@ -956,7 +961,10 @@ nau_status nau_set_mode(nau_ctx* c, int mode) {
 int nau_get_mode(nau_ctx* c) { return c->mode; }
 
 nau_status nau_set_neighbor_lists(nau_ctx* c, int on) {
+    if (on < 0 || on > 2) return fail(c, NAU_ERR_ARG, "neighbour list mode must be 0, 1 or 2");
     c->use_nlist = on != 0;
+    c->use_pairs = on == 1;
+    c->nl_rev = -1;
     return NAU_OK;
 }
 

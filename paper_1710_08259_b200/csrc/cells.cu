@@ -234,14 +234,41 @@ __global__ void __launch_bounds__(kSweepThreads) k_nlist(const __grid_constant__
     if (k >= *g.nact) return;
     uint2* lst = reinterpret_cast<uint2*>(list) + nlist_base(k, cap);
     const float pre_r = (float)radius;
-    int cnt, nrec = 0;
+    int cnt = 0, nrec = 0;
+    auto emit = [&](uint32_t v, uint32_t m) { emit_rec(lst, cap, nrec, cnt, v, m); };
     if (hg.on && *hg.escaped == 0)
-        cnt = build_list_half<DIM, ORDERED>(g, hg, k, lst, cap, nrec);
+        build_list_half<DIM, ORDERED>(g, hg, k, emit);
+    else if (axis_mode(g, radius) < 2)
+        build_list<DIM, ORDERED, false>(g, xl, k, pre_r, emit);
     else
-        cnt = axis_mode(g, radius) < 2
-                  ? build_list<DIM, ORDERED, false>(g, xl, k, pre_r, lst, cap, nrec)
-                  : build_list<DIM, ORDERED, true>(g, xl, k, pre_r, lst, cap, nrec);
+        build_list<DIM, ORDERED, true>(g, xl, k, pre_r, emit);
     count[k] = cnt;
+    if (nrec > cap) atomicMax(over, nrec);
+}
+
+// Paired lists (sweep.cuh consume_pairs): thread t = slots 2t, 2t+1; count[t] =
+// entries of the union of both masks.
+template <int DIM>
+__global__ void __launch_bounds__(kSweepThreads) k_nlist_pair(const __grid_constant__ Geo g,
+                                                              const float4* xl, double radius,
+                                                              uint32_t* list, int* count, int cap,
+                                                              int* over,
+                                                              const __grid_constant__ HalfGrid hg) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nact = *g.nact;
+    const int k0 = 2 * t;
+    if (k0 >= nact) return;
+    uint4* lst = reinterpret_cast<uint4*>(list) + (size_t)(t >> 5) * cap * 32 + (t & 31);
+    int cnt = 0, nrec = 0;
+    build_pair_list<DIM>(g, xl, hg, radius, k0, k0 + 1 < nact,
+                         [&](uint32_t v, uint32_t m0, uint32_t m1) {
+        if (m0 | m1) {
+            if (nrec < cap) st_rec4(lst, (unsigned)nrec, v, m0, m1);
+            ++nrec;
+            cnt += __popc(m0 | m1);
+        }
+    });
+    count[t] = cnt;
     if (nrec > cap) atomicMax(over, nrec);
 }
 
@@ -425,7 +452,7 @@ static HalfGrid half_grid(nau_ctx* c, double radius) {
     return hg;
 }
 
-bool build_nlist(nau_ctx* c, double radius, bool ordered) {
+bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs) {
     const long n = c->n;
     if (n == 0 || !c->use_nlist) return false;
     constexpr int kMaxCap = 1024;  // records per slot; beyond this sweeping is cheaper
@@ -444,8 +471,10 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered) {
     const int b = blocks_for(n, T);
     const HalfGrid hg = half_grid(c, radius);
     for (int attempt = 0; attempt < 3; ++attempt) {
-        // uint2 records + two slack rows (consume_list reads two records ahead)
-        const size_t need = slots * (size_t)c->nl_cap * 2 + 128;
+        // uint2 records + two slack rows (consume_list reads two records ahead);
+        // paired: uint4 records per thread pair + one slack row
+        const size_t need = pairs ? ((size_t)(n + 63) / 64 * 32) * c->nl_cap * 4 + 128
+                                  : slots * (size_t)c->nl_cap * 2 + 128;
         if (c->nl_len < need) {
             if (c->d_nlist) cudaFree(c->d_nlist);
             c->d_nlist = nullptr;
@@ -459,7 +488,14 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered) {
         cudaMemsetAsync(c->d_nover, 0, sizeof(int), c->stream);
         const double r = radius;
         prof_begin(c, 302);
-        if (ordered) {
+        if (pairs) {
+            const int pb = (int)(((n + 1) / 2 + T - 1) / T);
+            switch (c->dom.dim) {
+                case 1: k_nlist_pair<1><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
+                case 2: k_nlist_pair<2><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
+                default: k_nlist_pair<3><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
+            }
+        } else if (ordered) {
             switch (c->dom.dim) {
                 case 1: k_nlist<1, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
                 case 2: k_nlist<2, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
@@ -484,16 +520,22 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered) {
     return false;
 }
 
-bool nlist_for(nau_ctx* c, double radius, bool ordered) {
-    if (!c->use_nlist || c->n == 0) return false;
-    if (c->nl_rev == c->rebuild_count && c->nl_radius == radius && c->nl_ordered == ordered)
-        return true;
+int nlist_for(nau_ctx* c, double radius, bool ordered, bool pairs) {
+    if (!c->use_nlist || c->n == 0) return 0;
+    pairs = pairs && c->use_pairs && !ordered;
+    if (c->nl_rev == c->rebuild_count && c->nl_radius == radius && c->nl_ordered == ordered &&
+        c->nl_pairs == pairs)
+        return pairs ? 2 : 1;
     c->nl_rev = -1;
-    if (!build_nlist(c, radius, ordered)) return false;
+    if (!build_nlist(c, radius, ordered, pairs)) {
+        if (!pairs || !build_nlist(c, radius, ordered, false)) return 0;
+        pairs = false;
+    }
     c->nl_rev = c->rebuild_count;
     c->nl_radius = radius;
     c->nl_ordered = ordered;
-    return true;
+    c->nl_pairs = pairs;
+    return pairs ? 2 : 1;
 }
 
 void launch_unsort(nau_ctx* c, const double* d_src, double* d_dst, int comps) {

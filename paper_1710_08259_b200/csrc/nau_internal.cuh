@@ -364,6 +364,8 @@ struct nau_ctx {
     long nl_rev = -1;        // list cache key: cell build, radius, option order
     double nl_radius = 0.0;
     bool nl_ordered = false;
+    bool nl_pairs = false;   // paired layout (sweep.cuh consume_pairs)
+    bool use_pairs = true;
     // fp16 cell-relative coordinates in a cell-padded layout (sweep.cuh HalfGrid),
     // rebuilt lazily after each cell build
     __half* d_hq = nullptr;  // 3 x hq_len
@@ -424,10 +426,11 @@ void prof_end(nau_ctx* c, int cls);
 void launch_boundary_shift(nau_ctx* c);
 void launch_build_cells(nau_ctx* c);
 void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig);
-bool build_nlist(nau_ctx* c, double radius, bool ordered);  // false: lists unusable this step
-// The current cell build's list for (radius, order), built on first use and shared
-// by every neighbour pass until the cells are rebuilt.
-bool nlist_for(nau_ctx* c, double radius, bool ordered);
+bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs = false);  // false: unusable
+// The current cell build's list for (radius, order, layout), built on first use
+// and shared by every neighbour pass until the cells are rebuilt. Returns 0 (no
+// list: sweep), 1 (per-slot lists) or 2 (paired lists, when `pairs`).
+int nlist_for(nau_ctx* c, double radius, bool ordered, bool pairs = false);
 void launch_unsort(nau_ctx* c, const double* d_src, double* d_dst, int comps);
 void launch_sort_in(nau_ctx* c, const double* d_src_orig, double* d_dst, int comps);
 // interact.cu
@@ -449,5 +452,5 @@ void launch_reduce(nau_ctx* c, int kind, const double* f, int comps, double* h_o
 bool fast_supports(int op, int a_rows, int a_cols, int dim);
 void launch_interact_fast(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, double* out,
                           int a_rows, bool lists = false);
-void launch_wcsph_fast(nau_ctx* c, const nau_wcsph_params* p, double4* vp, bool lists);
+void launch_wcsph_fast(nau_ctx* c, const nau_wcsph_params* p, double4* vp, int lists);
 }  // namespace nau

@@ -320,9 +320,11 @@ __device__ __forceinline__ void emit_rec(uint2* rec, int cap, int& nrec, int& cn
     }
 }
 
-template <int DIM, bool ORDERED, bool AXIS>
-__device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict__ xl4, int k,
-                                          float pre_r, uint2* lst, int cap, int& nrec) {
+// emit(v, m) receives every 32-candidate block in candidate order: v = first
+// slot | image code << kSlotBits, m = survivor mask (possibly 0).
+template <int DIM, bool ORDERED, bool AXIS, class Emit>
+__device__ __forceinline__ void build_list(const Geo& g, const float4* __restrict__ xl4, int k,
+                                           float pre_r, Emit&& emit) {
     const DomainDev& d = g.dom;
     int ci[3] = {0, 0, 0};
     decode_cell<DIM>(d, g.key[k], ci);
@@ -337,7 +339,7 @@ __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict
     const float r2lim = rl * rl;
     const int n01 = ao[0].cnt * (DIM > 1 ? ao[1].cnt : 1);
     const int ncombo = n01 * (DIM > 2 ? ao[2].cnt : 1);
-    int cnt = 0;
+    
     for (int idx = 0; idx < ncombo; ++idx) {
         const int combo = ORDERED ? idx : ((idx & 1) ? ncombo - 1 - (idx >> 1) : (idx >> 1));
         const int o0 = combo % ao[0].cnt;
@@ -402,10 +404,9 @@ __device__ __forceinline__ int build_list(const Geo& g, const float4* __restrict
                 }
             }
             if (nb < 32) m &= (1u << nb) - 1u;
-            emit_rec(lst, cap, nrec, cnt, (uint32_t)t | icode, m);
+            emit((uint32_t)t | icode, m);
         }
     }
-    return cnt;
 }
 
 // Evaluate fn(j, rel, mask, payload) over a slot's list, payload = load(j) (the
@@ -603,11 +604,13 @@ __device__ __forceinline__ float half_offset(const AxisOpts& ao, int ci, int o, 
     return 2.0f;
 }
 
-template <int DIM, bool ORDERED>
-__device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg, int k,
-                                               uint2* lst, int cap, int& nrec) {
+// NP (1 or 2) particles of ONE cell share the option sequence and every
+// coordinate load; each gets its own mask: emit(v, m) with m[NP].
+template <int DIM, bool ORDERED, int NP, class Emit>
+__device__ __forceinline__ void half_scan(const Geo& g, const HalfGrid& hg, const int* ks,
+                                          Emit&& emit) {
     const DomainDev& d = g.dom;
-    const int flat_i = g.key[k];
+    const int flat_i = g.key[ks[0]];
     int ci[3] = {0, 0, 0};
     decode_cell<DIM>(d, flat_i, ci);
     AxisOpts ao[3];
@@ -615,11 +618,14 @@ __device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg,
     for (int a = 0; a < 3; ++a) ao[a] = AxisOpts{0, 1, 1};
 #pragma unroll
     for (int a = 0; a < DIM; ++a) ao[a] = axis_opts(d, a, ci[a]);
-    const int rk = k - g.cell_start[flat_i];  // rank in the cell -> interleaved position
-    const int pk = hg.pstart[flat_i] + (rk & ~31) + 2 * (rk & 15) + ((rk >> 4) & 1);
-    float hi[3] = {0.f, 0.f, 0.f};
+    float hi[NP][3];
 #pragma unroll
-    for (int a = 0; a < DIM; ++a) hi[a] = __half2float(hg.h[a][pk]);
+    for (int p = 0; p < NP; ++p) {
+        const int rk = ks[p] - g.cell_start[flat_i];  // rank in the cell -> interleaved position
+        const int pk = hg.pstart[flat_i] + (rk & ~31) + 2 * (rk & 15) + ((rk >> 4) & 1);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) hi[p][a] = a < DIM ? __half2float(hg.h[a][pk]) : 0.f;
+    }
     const float rl = hg.rho + 0.0022f;
     const __half2 nlim2 = __hneg2(__half2half2(__float2half_ru(fmaf(rl, rl, 0.003f))));
     const int n01 = ao[0].cnt * (DIM > 1 ? ao[1].cnt : 1);
@@ -627,7 +633,7 @@ __device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg,
     // option setup; the next option's cell-table reads are issued one option
     // ahead (a lane's 27 options are otherwise a chain of dependent latencies)
     struct Opt {
-        __half2 sg2[3], bq2[3];
+        __half2 sg2[3], bq2[NP][3];
         uint32_t icode;
         int s, ns, ps;
     };
@@ -642,7 +648,8 @@ __device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg,
             int ic, cell;
             const float off = half_offset(ao[a], ci[a], oo[a], sg, ic, cell, d.cells[a], d.kind[a]);
             o.sg2[a] = __float2half2_rn(sg);
-            o.bq2[a] = __float2half2_rn(off - hi[a]);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) o.bq2[p][a] = __float2half2_rn(off - hi[p][a]);
             flat += stride * cell;
             code += scode * ic;
             stride *= d.cells[a];
@@ -653,36 +660,40 @@ __device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg,
         o.ns = g.cell_count[flat];
         o.ps = hg.pstart[flat];
     };
-    int cnt = 0;
     Opt nxt;
     setup(0, nxt);
     for (int idx = 0; idx < ncombo; ++idx) {
         const Opt o = nxt;
         if (idx + 1 < ncombo) setup(idx + 1, nxt);
         for (int q0 = 0; q0 < o.ns; q0 += 32) {
-            // all four 8-candidate groups loaded up front (the padded layout has
-            // slack past the last cell; lanes past the cell are masked below)
+            // the whole 32-slot block of each axis up front (cells are padded
+            // to 32 slots with +inf)
             uint4 hv[4][3];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
                 for (int a = 0; a < DIM; ++a)
                     hv[u][a] = *reinterpret_cast<const uint4*>(hg.h[a] + o.ps + q0 + 8 * u);
-            uint32_t m = 0;
+            uint32_t m[NP];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) m[p] = 0;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t* w[3] = {&hv[u][0].x, &hv[u][1].x, &hv[u][2].x};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    __half2 dd = nlim2;
-#pragma unroll
-                    for (int a = 0; a < DIM; ++a) {
-                        const __half2 x2 = *reinterpret_cast<const __half2*>(w[a] + q);
-                        const __half2 r = __hfma2(o.sg2[a], x2, o.bq2[a]);
-                        dd = __hfma2(r, r, dd);
-                    }
                     const int kw = 4 * u + q;  // word kw: candidates kw, kw + 16
-                    m += (*reinterpret_cast<const uint32_t*>(&dd) & 0x80008000u) >> (15 - kw);
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        __half2 dd = nlim2;
+#pragma unroll
+                        for (int a = 0; a < DIM; ++a) {
+                            const __half2 x2 = *reinterpret_cast<const __half2*>(w[a] + q);
+                            const __half2 r = __hfma2(o.sg2[a], x2, o.bq2[p][a]);
+                            dd = __hfma2(r, r, dd);
+                        }
+                        m[p] += (*reinterpret_cast<const uint32_t*>(&dd) & 0x80008000u) >> (15 - kw);
+                    }
                 }
             }
             if (q0 == 0 && idx + 1 < ncombo) {
@@ -690,16 +701,23 @@ __device__ __forceinline__ int build_list_half(const Geo& g, const HalfGrid& hg,
                 // is expanded (an L1 miss on a block's loads stalls the whole block)
 #pragma unroll
                 for (int a = 0; a < DIM; ++a) {
-                    const __half* p = hg.h[a] + nxt.ps;
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-                    if (nxt.ns > 56) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 64));
+                    const __half* pp = hg.h[a] + nxt.ps;
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(pp));
+                    if (nxt.ns > 56) asm volatile("prefetch.global.L1 [%0];" ::"l"(pp + 64));
                 }
             }
-            if (o.ns - q0 < 32) m &= (1u << (o.ns - q0)) - 1u;
-            emit_rec(lst, cap, nrec, cnt, (uint32_t)(o.s + q0) | o.icode, m);
+            if (o.ns - q0 < 32)
+#pragma unroll
+                for (int p = 0; p < NP; ++p) m[p] &= (1u << (o.ns - q0)) - 1u;
+            emit((uint32_t)(o.s + q0) | o.icode, m);
         }
     }
-    return cnt;
+}
+
+template <int DIM, bool ORDERED, class Emit>
+__device__ __forceinline__ void build_list_half(const Geo& g, const HalfGrid& hg, int k,
+                                                Emit&& emit) {
+    half_scan<DIM, ORDERED, 1>(g, hg, &k, [&](uint32_t v, const uint32_t* m) { emit(v, m[0]); });
 }
 
 struct NList {  // per-step neighbour lists (k_nlist in cells.cu): chunk records
@@ -739,6 +757,119 @@ __device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __rest
     } else {
         sweep<DIM, ORDERED>(g, xl4, k, valid, xi, radius,
                             [&](int j, const double* rel, int mask) { fn(j, rel, mask, load(j)); });
+    }
+}
+
+// ---- paired lists (FAST WCSPH deck) -------------------------------------------
+// Thread t owns slots 2t and 2t+1. When both sit in one cell (all but ~1 in 64
+// pairs at the BASELINE decks) they share the option sequence, so one record
+// per 32-candidate block carries both survivor masks: (first slot | image code,
+// m0, m1) as a uint4. The consumer walks the union of the masks; every gathered
+// neighbour (position + payload) serves both particles, each contribution
+// selected by its own bit — the gathers, which bound the per-slot consumers in
+// L1, are shared, and the two particles' arithmetic runs as two independent
+// chains. Pairs that straddle a cell boundary store the first particle's blocks
+// (m1 = 0), then the second's (m0 = 0). Each particle still visits its own
+// candidates in the sweep's order: the same sums as the per-slot lists.
+__device__ __forceinline__ void st_rec4(uint4* base, unsigned r, uint32_t v, uint32_t m0,
+                                        uint32_t m1) {
+    asm volatile(
+        "{\n\t.reg .u64 a;\n\t"
+        "mad.wide.u32 a, %1, 512, %0;\n\t"
+        "st.global.v4.u32 [a], {%2, %3, %4, %5};\n\t}"
+        :
+        : "l"(base), "r"(r), "r"(v), "r"(m0), "r"(m1), "r"(m0 | m1)
+        : "memory");
+}
+
+// Records of a thread pair; fn(v, m0, m1) per block as in build_list.
+template <int DIM, class Emit2>
+__device__ __forceinline__ void build_pair_list(const Geo& g, const float4* __restrict__ xl4,
+                                                const HalfGrid& hg, double radius, int k0,
+                                                bool has1, Emit2&& emit2) {
+    const int k1 = k0 + 1;
+    if (hg.on && *hg.escaped == 0) {
+        if (has1 && g.key[k0] == g.key[k1]) {
+            const int ks[2] = {k0, k1};
+            half_scan<DIM, false, 2>(g, hg, ks,
+                                     [&](uint32_t v, const uint32_t* m) { emit2(v, m[0], m[1]); });
+        } else {
+            build_list_half<DIM, false>(g, hg, k0, [&](uint32_t v, uint32_t m) { emit2(v, m, 0u); });
+            if (has1)
+                build_list_half<DIM, false>(g, hg, k1,
+                                            [&](uint32_t v, uint32_t m) { emit2(v, 0u, m); });
+        }
+        return;
+    }
+    const float pre_r = (float)radius;
+    auto one = [&](int k, bool second) {
+        auto e = [&](uint32_t v, uint32_t m) { second ? emit2(v, 0u, m) : emit2(v, m, 0u); };
+        if (axis_mode(g, radius) < 2)
+            build_list<DIM, false, false>(g, xl4, k, pre_r, e);
+        else
+            build_list<DIM, false, true>(g, xl4, k, pre_r, e);
+    };
+    one(k0, false);
+    if (has1) one(k1, true);
+}
+
+// fn(j, xj_image, image_mask, live0, live1, payload) for the union of the two
+// particles' candidates; IMG = false: no periodic / symmetric axis.
+template <int DIM, bool IMG, class Load, class Fn>
+__device__ __forceinline__ void consume_pairs(const Geo& g, const uint4* __restrict__ rec,
+                                              int cnt, Load&& load, Fn&& fn) {
+    constexpr uint32_t kM = (1u << kSlotBits) - 1;
+    using P = decltype(load(0));
+    struct Buf {
+        uint32_t ent, fl;
+        double4 p;
+        P pl;
+    };
+    uint4 cur = rec[0], n1 = rec[32];  // (v, m0, m1, m0 | m1 remaining)
+    int r = 0;
+    auto gen = [&](uint32_t& fl) -> uint32_t {
+        const bool sw = cur.w == 0;
+        cur.x = sw ? n1.x : cur.x;
+        cur.y = sw ? n1.y : cur.y;
+        cur.z = sw ? n1.z : cur.z;
+        cur.w = sw ? n1.w : cur.w;
+        r += sw;
+        if (sw) n1 = rec[(r + 1) * 32];  // at most record `nrec`: the slack row
+        const uint32_t b = (uint32_t)(__ffs(cur.w) - 1);
+        cur.w &= cur.w - 1;
+        fl = ((cur.y >> b) & 1u) | (((cur.z >> b) & 1u) << 1);
+        return cur.x + b;
+    };
+    auto fetch = [&](Buf& b, int s) {
+        b.fl = 0;
+        b.ent = s < cnt ? gen(b.fl) : 0u;
+        b.p = ld256(g.p4 + (b.ent & kM));
+        b.pl = load((int)(b.ent & kM));
+    };
+    auto process = [&](const Buf& b) {
+        const int j = (int)(b.ent & kM);
+        double xj[3] = {b.p.x, b.p.y, b.p.z};
+        int mask = 0;
+        if constexpr (IMG) {
+            const int c = (int)(b.ent >> kSlotBits);
+            if (c != 0) {
+                const int cc[3] = {c % 5, (c / 5) % 5, c / 25};
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    xj[a] = image_of(g.img[a], xj[a], cc[a]);
+                    mask |= (cc[a] >= 3) << a;
+                }
+            }
+        }
+        fn(j, xj, mask, (b.fl & 1u) != 0, (b.fl & 2u) != 0, b.pl);
+    };
+    Buf A, B;
+    fetch(A, 0);
+    for (int s = 0; s < cnt; s += 2) {
+        fetch(B, s + 1);
+        process(A);
+        fetch(A, s + 2);
+        process(B);  // past the end: fl = 0, both contributions deselected
     }
 }
 

@@ -361,9 +361,10 @@ class Context:
     def fast(self):
         return self.L.nau_get_mode(self.h) == MODE_FAST
 
-    def set_neighbor_lists(self, on: bool):
-        """Per-step neighbour lists for wcsph_step (identical results, faster)."""
-        self._check(self.L.nau_set_neighbor_lists(self.h, 1 if on else 0))
+    def set_neighbor_lists(self, on):
+        """Per-step neighbour lists (identical results, faster): False/0 off, True/1 on
+        (paired lists for the FAST Wendland wcsph_step), 2 on with per-particle lists only."""
+        self._check(self.L.nau_set_neighbor_lists(self.h, int(on)))
 
     def set_stream(self, stream_ptr):
         self._check(self.L.nau_set_stream(self.h, C.c_void_p(stream_ptr)))

@@ -472,11 +472,12 @@ def test_neighbor_lists_identical_to_sweep_dam3d(fast):
     """The per-step lists visit the sweep's candidates in the sweep's order: bitwise
     identical results with lists on and off (3D dam break, both modes)."""
     build = lambda c: _gpu_dam(c, scenes.dam_break(3, dx=0.02))
-    on, act_on = _run_deck(build, fast, True, 3)
-    off, act_off = _run_deck(build, fast, False, 3)
-    np.testing.assert_array_equal(act_on, act_off)
-    for k in on:
-        np.testing.assert_array_equal(on[k], off[k], err_msg=k)
+    off, act_off = _run_deck(build, fast, 0, 3)
+    for mode in (1, 2):  # paired lists (FAST), per-particle lists
+        on, act_on = _run_deck(build, fast, mode, 3)
+        np.testing.assert_array_equal(act_on, act_off)
+        for k in on:
+            np.testing.assert_array_equal(on[k], off[k], err_msg=(mode, k))
 
 
 @pytest.mark.parametrize("n,radius,kind,outside", [(8000, 0.25, nau.PERIODIC, 0),
@@ -491,10 +492,11 @@ def test_neighbor_lists_capacity_growth_and_fallback(n, radius, kind, outside):
     box (fp16 pre-filter disabled at run time)."""
     build = _random_deck(n, 77, kind, radius, outside)
     for fast in (False, True):
-        on, _ = _run_deck(build, fast, True, 2)
-        off, _ = _run_deck(build, fast, False, 2)
-        for k in on:
-            np.testing.assert_array_equal(on[k], off[k], err_msg=(fast, k))
+        off, _ = _run_deck(build, fast, 0, 2)
+        for mode in ((1, 2) if fast else (1,)):
+            on, _ = _run_deck(build, fast, mode, 2)
+            for k in on:
+                np.testing.assert_array_equal(on[k], off[k], err_msg=(fast, mode, k))
 
 
 # ------------------------------------------- device SFL evaluator (§8(f) 1) ----
