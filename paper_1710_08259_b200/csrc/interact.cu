@@ -480,7 +480,10 @@ __global__ void __launch_bounds__(kGravTile) k_gravity(const __grid_constant__ G
 // test: rel = 0 there, so it adds exactly zero (r2 = eps^2 > 0 keeps it finite).
 // Per pair: 3 DADD + 3 DFMA + rsqrt + 3 DMUL + 3 DFMA and a quarter of a shared
 // load — profiles/r1b: the one-body loop issued 45 instructions per pair.
-constexpr int kGravBodies = 2;
+#ifndef NAU_GRAV_BODIES
+#define NAU_GRAV_BODIES 2
+#endif
+constexpr int kGravBodies = NAU_GRAV_BODIES;
 constexpr int kGravThreads = 128;
 
 template <int DIM>
@@ -532,8 +535,16 @@ __global__ void __launch_bounds__(kGravThreads) k_gravity_fast(const __grid_cons
                     rel[d] = xj[d] - xi[b][d];
                     r2 = fma(rel[d], rel[d], r2);
                 }
-                const double inv = rsqrt(r2);
-                const double s = sj.w * (inv * (inv * inv));
+                // m / r^3 from the MUFU estimate y ~ 1/sqrt(r2) (r2 >= eps2 > 0, normal):
+                // with e = 1 - r2 y^2, r2^(-3/2) = y^3 (1 - e)^(-3/2)
+                //   = y^3 (1 + 3e/2 + 15e^2/8 + O(e^3)),  |e| < 2^-19 (tools/mufu_acc.cu),
+                // no special-value branch (CUDA's rsqrt) and one FP64 op fewer than
+                // rsqrt + two products
+                double y;
+                asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+                const double y2 = y * y;
+                const double e = fma(-r2, y2, 1.0);
+                const double s = ((sj.w * y) * y2) * fma(e, fma(1.875, e, 1.5), 1.0);
 #pragma unroll
                 for (int d = 0; d < DIM; ++d) acc[b][d] = fma(rel[d], s, acc[b][d]);
             }
@@ -642,7 +653,7 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
         prof_begin(c, 100 + op);
         const bool fast = c->mode == NAU_MODE_FAST;
         const bool uniform_soft = a.G.p == nullptr && a.has_eps && a.eps.p == nullptr &&
-                                  a.eps.v[0] * a.eps.v[0] > 0.0;
+                                  a.eps.v[0] * a.eps.v[0] >= 1e-300;  // normal: MUFU is ftz
         if (fast && uniform_soft) {
             const int nb = (int)((c->n + kGravThreads * kGravBodies - 1) / (kGravThreads * kGravBodies));
             const double G = a.G.v[0], eps2 = a.eps.v[0] * a.eps.v[0];

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build experimental variants of libnau_b200.so (extra -D flags on the list
-# consumers / FAST kernels) into build/var/<name>/; select one at run time with
+# consumers / FAST kernels / interactions) into build/var/<name>/; select one at run time with
 # NAU_LIB=build/var/<name>/libnau_b200.so. Usage: tools/variants.sh name "-DFOO=1" ...
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
@@ -13,8 +13,9 @@ while [ $# -ge 2 ]; do
   out=$ROOT/build/var/$name; mkdir -p "$out"
   ( nvcc $FLAGS $defs -Xptxas -v -c "$CS/fast.cu" -o "$out/fast.o" 2> "$out/fast.ptxas.txt" &&
     nvcc $FLAGS -fmad=false $defs -c "$CS/cells.cu" -o "$out/cells.o" &&
-    objs=$(ls $ROOT/build/csrc/*.o | grep -v -e /fast.o -e /cells.o) &&
-    nvcc $ARCH -shared -o "$out/libnau_b200.so" "$out/fast.o" "$out/cells.o" $objs -lcudart &&
+    nvcc $FLAGS -fmad=false $defs -c "$CS/interact.cu" -o "$out/interact.o" &&
+    objs=$(ls $ROOT/build/csrc/*.o | grep -v -e /fast.o -e /cells.o -e /interact.o) &&
+    nvcc $ARCH -shared -o "$out/libnau_b200.so" "$out/fast.o" "$out/cells.o" "$out/interact.o" $objs -lcudart -ldl &&
     echo "built $name" ) &
 done
 wait
