@@ -351,6 +351,8 @@ void nau_destroy(nau_ctx* c) {
     dfree(c->d_nlist);
     dfree(c->d_ncount);
     dfree(c->d_nover);
+    if (c->h_nover) cudaFreeHost(c->h_nover);
+    c->h_nover = c->h_nover_dev = nullptr;
     dfree(c->d_hq);
     dfree(c->d_pstart);
     dfree(c->d_pcount);

@@ -452,6 +452,8 @@ static HalfGrid half_grid(nau_ctx* c, double radius) {
     return hg;
 }
 
+static __global__ void k_publish(const int* src, int* dst) { *(volatile int*)dst = *src; }
+
 bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs) {
     const long n = c->n;
     if (n == 0 || !c->use_nlist) return false;
@@ -459,6 +461,15 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs) {
     const size_t slots = (size_t)((n + 31) / 32) * 32;
     if (c->nl_cap == 0) c->nl_cap = 64;
     if (!c->d_nover && cudaMalloc(&c->d_nover, sizeof(int)) != cudaSuccess) return false;
+    if (!c->h_nover) {
+        if (cudaHostAlloc(&c->h_nover, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+            cudaHostGetDevicePointer(&c->h_nover_dev, c->h_nover, 0) != cudaSuccess) {
+            cudaGetLastError();
+            if (c->h_nover) cudaFreeHost(c->h_nover);
+            c->h_nover = c->h_nover_dev = nullptr;
+            return false;
+        }
+    }
     if (c->nc_len < n) {
         if (c->d_ncount) cudaFree(c->d_ncount);
         c->d_ncount = nullptr;
@@ -510,9 +521,13 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs) {
         }
         prof_end(c, 302);
         c->launches++;
-        int over = 0;
-        cudaMemcpyAsync(&over, c->d_nover, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+        // The overflow word reaches the host through mapped memory written by a
+        // one-thread kernel: a cudaMemcpy would queue on the D2H copy engine behind
+        // the previous step's result downloads and stall the step until they finish.
+        k_publish<<<1, 1, 0, c->stream>>>(c->d_nover, c->h_nover_dev);
+        c->launches++;
         if (cudaStreamSynchronize(c->stream) != cudaSuccess) return false;
+        const int over = *(volatile int*)c->h_nover;
         if (over == 0) return true;
         if (over > kMaxCap) return false;
         c->nl_cap = std::min(kMaxCap, ((over + over / 4 + 31) / 32) * 32);

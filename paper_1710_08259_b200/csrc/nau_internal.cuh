@@ -360,6 +360,8 @@ struct nau_ctx {
     int* d_ncount = nullptr;
     long nc_len = 0;
     int* d_nover = nullptr;  // max list length seen when > cap (0 = fits)
+    int* h_nover = nullptr;  // its host copy: mapped pinned memory written by a kernel (no copy engine)
+    int* h_nover_dev = nullptr;
     int nl_cap = 0;
     long nl_rev = -1;        // list cache key: cell build, radius, option order
     double nl_radius = 0.0;
