@@ -1,0 +1,22 @@
+# Round evidence on one B200: bench lines for every BASELINE config, cfg2 EXACT and the
+# reference arm, ncu launch lists (cfg2 bench, cfg4 step) and full captures.
+# usage: bash tools/measure_round.sh TAG   (outputs in gpurun_out/TAG_*)
+T=${1:-r1e}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_throttle_reasons.active --format=csv,noheader
+for c in 2 0 1 3 4; do
+  timeout 900 python bench.py --config $c > gpurun_out/${T}_bench_cfg$c.json 2> gpurun_out/${T}_bench_cfg$c.err
+  echo "cfg$c rc=$?"; tail -c 300 gpurun_out/${T}_bench_cfg$c.json
+done
+timeout 900 python bench.py --config 2 --mode exact --no-cpu-baseline > gpurun_out/${T}_bench_cfg2_exact.json 2> gpurun_out/${T}_bench_cfg2_exact.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${T}_reference_cfg2.json 2> gpurun_out/${T}_reference_cfg2.err
+echo "ref rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/${T}_launches_cfg2.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/${T}_ncu_launch2.log 2>&1
+echo "launches2 rc=$?"
+timeout 600 python tools/profile_step.py --config 4 --steps 1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/${T}_launches_cfg4.csv python tools/profile_step.py --config 4 --steps 1 > gpurun_out/${T}_ncu_launch4.log 2>&1
+echo "launches4 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gravity_fast -c 1 \
+  -o gpurun_out/${T}_full_cfg4 python tools/profile_step.py --config 4 --steps 1 > gpurun_out/${T}_ncu_full4.log 2>&1
+echo "full4 rc=$?"
