@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_neighbor_counts(Geo g, const 
     double xi[3] = {0.0, 0.0, 0.0};
     for (int a = 0; a < DIM; ++a) xi[a] = g.x[a * g.n + kk];
     int cnt = 0;
-    sweep<DIM, false>(g, xl, k, valid, xi, radius,
+    sweep<DIM, false, true>(g, xl, k, valid, xi, radius,  // order-free count: rows
                [&](int, const double* rel, int) {
         if (norm_rel<DIM>(rel) <= radius) ++cnt;
     });

@@ -34,6 +34,9 @@
 
 namespace nau {
 
+#ifndef NAU_ROWS
+#define NAU_ROWS 1
+#endif
 constexpr int kQueue = 64;          // FIFO depth per lane (8 KB of shared memory per warp)
 constexpr int kChunk = 16;          // max candidates scanned between warp votes
 constexpr int kSweepThreads = 128;  // 4 warps, 32 KB shared memory per CTA
@@ -108,7 +111,7 @@ __device__ __forceinline__ int axis_mode(const Geo& g, double radius) {
 // The sweep. Must be called by all 32 lanes of a warp (valid = false for lanes
 // without a particle). `pre_r` is the pre-filter radius (>= the operator's
 // acceptance radius).
-template <int DIM, bool ORDERED, int AX, class Fn>
+template <int DIM, bool ORDERED, int AX, bool ROWS, class Fn>
 __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restrict__ xl4, int k,
                                            bool valid, const double* xi, float pre_r,
                                            SweepSmem& sm, Fn& fn) {
@@ -132,7 +135,17 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
     }
     const float rl = pre_r * 1.001f + g.pre_abs;
     const float r2lim = rl * rl;
-    const int n01 = ao[0].cnt * (DIM > 1 ? ao[1].cnt : 1);
+    // ROWS: the direct axis-0 options of one (o1, o2) are consecutive flat cells, so
+    // their candidates form ONE contiguous slot range (slots are ordered by flat
+    // cell) unless a periodic wrap splits them: one super-option per row instead of
+    // up to three, mirror options after it as before. The odometer order (axis 0
+    // fastest, direct cells then mirrors) is unchanged, so ORDERED sums stay
+    // bitwise; at ~3 particles per cell (cfg3) the per-option setup and its two
+    // dependent table loads were most of the sweep.
+    const bool row = NAU_ROWS && ROWS && valid &&
+                     (d.kind[0] != NAU_PERIODIC || (ci[0] >= 1 && ci[0] + 1 < d.cells[0]));
+    const int cnt0 = row ? 1 + ao[0].cnt - ao[0].ndir : ao[0].cnt;
+    const int n01 = cnt0 * (DIM > 1 ? ao[1].cnt : 1);
     const int ncombo = n01 * (DIM > 2 ? ao[2].cnt : 1);
     int idx = -1;  // position in the option sequence
     int t = 0, e = 0;
@@ -147,12 +160,21 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
                 return;
             }
             const int combo = ORDERED ? idx : ((idx & 1) ? ncombo - 1 - (idx >> 1) : (idx >> 1));
-            const int o0 = combo % ao[0].cnt;
-            const int o1 = DIM > 1 ? (combo / ao[0].cnt) % ao[1].cnt : 0;
+            const int o0 = combo % cnt0;
+            const int o1 = DIM > 1 ? (combo / cnt0) % ao[1].cnt : 0;
             const int o2 = DIM > 2 ? combo / n01 : 0;
             int cell, ic;
             float bs;
-            option_of(d, 0, ci[0], ao[0], o0, cell, ic, sg[0], bs);
+            int row_last = 0;  // cells merged after `cell` along axis 0
+            if (row && o0 == 0) {
+                cell = ci[0] + ao[0].lo_off;
+                ic = 0;
+                sg[0] = 1.0f;
+                bs = 0.0f;
+                row_last = ao[0].ndir - 1;
+            } else {
+                option_of(d, 0, ci[0], ao[0], row ? ao[0].ndir + o0 - 1 : o0, cell, ic, sg[0], bs);
+            }
             int flat = cell;
             int code = ic;
             bq[0] = bs - xli[0];
@@ -170,7 +192,8 @@ __device__ __forceinline__ void sweep_impl(const Geo& g, const float4* __restric
             }
             icode = (uint32_t)code << kSlotBits;
             t = g.cell_start[flat];
-            e = t + g.cell_count[flat];
+            e = row_last ? g.cell_start[flat + row_last] + g.cell_count[flat + row_last]
+                         : t + g.cell_count[flat];
         }
     };
     if (!done) advance();
@@ -534,7 +557,10 @@ struct Ld256 {
 // Entry point: `radius` is the lane's acceptance radius (fp64); the per-axis
 // mode is the warp's maximum of axis_mode (BASELINE decks: radius = cell size,
 // mode 1).
-template <int DIM, bool ORDERED, class Fn>
+// ROWS (default: ORDERED, where it keeps the order) merges each stencil row's direct
+// cells into one slot range; unordered callers opt in only where the summation
+// order is free (FAST SPH sweeps must match the lists' order).
+template <int DIM, bool ORDERED, bool ROWS = ORDERED, class Fn>
 __device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ xl4, int k,
                                       bool valid, const double* xi, double radius, Fn&& fn) {
     __shared__ SweepSmem smem[kSweepThreads / 32];
@@ -542,11 +568,11 @@ __device__ __forceinline__ void sweep(const Geo& g, const float4* __restrict__ x
     const float pre_r = (float)radius;
     const int ax = __reduce_max_sync(0xffffffffu, valid ? axis_mode(g, radius) : 0);
     if (ax == 0)
-        sweep_impl<DIM, ORDERED, 0>(g, xl4, k, valid, xi, pre_r, sm, fn);
+        sweep_impl<DIM, ORDERED, 0, ROWS>(g, xl4, k, valid, xi, pre_r, sm, fn);
     else if (ax == 1)
-        sweep_impl<DIM, ORDERED, 1>(g, xl4, k, valid, xi, pre_r, sm, fn);
+        sweep_impl<DIM, ORDERED, 1, ROWS>(g, xl4, k, valid, xi, pre_r, sm, fn);
     else
-        sweep_impl<DIM, ORDERED, 2>(g, xl4, k, valid, xi, pre_r, sm, fn);
+        sweep_impl<DIM, ORDERED, 2, ROWS>(g, xl4, k, valid, xi, pre_r, sm, fn);
 }
 
 // ---- half-precision pre-filter for the list build ------------------------------
