@@ -49,12 +49,17 @@ __global__ void k_boundary_shift(DomainDev d, long n, double* pos, uint8_t* acti
     if (warn) atomicAdd(&err->warnings, warn);
 }
 
+// AGG: one atomic per distinct cell per warp (__match_any_sync) — consecutive
+// slots mostly share a cell, so per-particle atomics serialise on one address
+// (cfg2, 64 per cell: hash + scatter 0.27 -> 0.17 ms); at a few particles per
+// cell the match costs more than it saves (cfg3: +5%), see build_cells.
+template <bool AGG>
 __global__ void k_hash(DomainDev d, long n, const double* pos, const uint8_t* active,
                        const int* orig, int* key, int* count, DevErr* err) {
-    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (k >= n) return;
+    const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    const bool valid = k < n;
     int flat = d.ncells;
-    if (active[k]) {
+    if (valid && active[k]) {
         flat = 0;
         for (int a = d.dim - 1; a >= 0; --a) {
             double x = pos[a * n + k];
@@ -63,8 +68,16 @@ __global__ void k_hash(DomainDev d, long n, const double* pos, const uint8_t* ac
             flat = flat * d.cells[a] + cell_index(d, a, x);
         }
     }
+    if (!AGG) {
+        if (!valid) return;
+        key[k] = flat;
+        atomicAdd(&count[flat], 1);
+        return;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, valid ? flat : -1);
+    if (!valid) return;
     key[k] = flat;
-    atomicAdd(&count[flat], 1);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[flat], __popc(peers));
 }
 
 // ---- exclusive scan of int32 (three-phase: tile scan, tile-sum scan, add) ----
@@ -139,12 +152,28 @@ __global__ void k_scan_add(int* out, long n, const int* tile_sums) {
         if (base + i < n) out[base + i] += add;
 }
 
+// AGG: warp-aggregated cursor, the lanes of one cell take consecutive slots after
+// one atomic (the within-cell order is fixed by k_rank afterwards).
+template <bool AGG>
 __global__ void k_scatter(long n, const int* key, const int* orig, const int* start, int* cursor,
                           int* perm_tmp, int* okey) {
-    long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    int c = key[k];
-    int slot = start[c] + atomicAdd(&cursor[c], 1);
+    const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    const bool valid = k < n;
+    const int c = valid ? key[k] : -1;
+    if (!AGG) {
+        if (!valid) return;
+        const int slot = start[c] + atomicAdd(&cursor[c], 1);
+        perm_tmp[slot] = (int)k;
+        okey[slot] = orig[k];
+        return;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, c);
+    const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+    int base = 0;
+    if (valid && lane == leader) base = atomicAdd(&cursor[c], __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (!valid) return;
+    const int slot = start[c] + base + __popc(peers & ((1u << lane) - 1u));
     perm_tmp[slot] = (int)k;
     okey[slot] = orig[k];
 }
@@ -346,17 +375,27 @@ void launch_build_cells(nau_ctx* c) {
     const int nc = c->dom.ncells;
     cudaMemsetAsync(c->d_cell_count, 0, sizeof(int) * (nc + 1), c->stream);
     cudaMemsetAsync(c->d_cursor, 0, sizeof(int) * (nc + 1), c->stream);
+    const bool agg = n >= 8L * nc;  // >= 8 particles per cell on average
     if (n > 0) {
-        k_hash<<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_active,
-                                                        c->d_orig, c->d_key, c->d_cell_count,
-                                                        c->d_err);
+        if (agg)
+            k_hash<true><<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_active,
+                                                                  c->d_orig, c->d_key, c->d_cell_count,
+                                                                  c->d_err);
+        else
+            k_hash<false><<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_active,
+                                                                   c->d_orig, c->d_key, c->d_cell_count,
+                                                                   c->d_err);
         c->launches++;
     }
     // cell_start[ncells] (start of the inactive tail bin) = number of active particles.
     scan_exclusive(c, c->d_cell_count, c->d_cell_start, nc + 1);
     if (n == 0) return;
-    k_scatter<<<blocks_for(n), kBlock, 0, c->stream>>>(n, c->d_key, c->d_skey, c->d_cell_start,
-                                                       c->d_cursor, c->d_perm_tmp, c->d_okey);
+    if (agg)
+        k_scatter<true><<<blocks_for(n), kBlock, 0, c->stream>>>(n, c->d_key, c->d_skey, c->d_cell_start,
+                                                                 c->d_cursor, c->d_perm_tmp, c->d_okey);
+    else
+        k_scatter<false><<<blocks_for(n), kBlock, 0, c->stream>>>(n, c->d_key, c->d_skey, c->d_cell_start,
+                                                                  c->d_cursor, c->d_perm_tmp, c->d_okey);
     // (okey = the within-cell sort key: original index, or a slab's global id)
     k_rank<<<blocks_for(n), kBlock, 0, c->stream>>>(n, nc, c->d_key, c->d_cell_start,
                                                     c->d_cell_count, c->d_perm_tmp, c->d_okey,
@@ -399,6 +438,9 @@ void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig) {
 
 // fp16 pre-filter data for the list build (sweep.cuh HalfGrid), rebuilt once per
 // cell build. Off (fp32 pre-filter) for anisotropic cells or radius > 1.5 cells.
+#ifndef NAU_HALF
+#define NAU_HALF 1
+#endif
 static HalfGrid half_grid(nau_ctx* c, double radius) {
     HalfGrid hg{};
     const DomainDev& d = c->dom;
@@ -406,7 +448,7 @@ static HalfGrid half_grid(nau_ctx* c, double radius) {
     bool iso = true;
     for (int a = 1; a < d.dim; ++a) iso &= d.cs[a] == d.cs[0];
     const double rho = radius / d.cs[0];
-    if (!iso || !(rho <= 1.5) || c->n == 0) return hg;
+    if (!NAU_HALF || !iso || !(rho <= 1.5) || c->n == 0) return hg;
     // cells padded to 32-slot blocks (only non-empty cells pad) plus slack
     const long hlen = ((c->n + 32L * std::min<long>(nc, c->n) + 64) + 7) & ~7L;
     if (c->hq_len < hlen) {
