@@ -183,7 +183,10 @@ struct DemArgs {
 };
 
 template <int DIM, int OP>
-__global__ void __launch_bounds__(kThreads) k_dem(const __grid_constant__ DemArgs a) {
+#ifndef NAU_DEM_MINB
+#define NAU_DEM_MINB 4  // <= 128 registers: 4 blocks/SM (136 regs: 3 blocks, +28%; 96 with spills: +18%)
+#endif
+__global__ void __launch_bounds__(kThreads, NAU_DEM_MINB) k_dem(const __grid_constant__ DemArgs a) {
     const Geo& g = a.g;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = k < *g.nact;
