@@ -212,6 +212,7 @@ def stencil_candidates(ctx, dim):
 class Workload:
     name = ""
     dtype = "f64"
+    survey = None  # (bytes, fp64 flops) per step by SURVEY.md §8(d)'s convention, basis
 
     def setup(self, ctx):
         raise NotImplementedError
@@ -255,6 +256,10 @@ class Microbench(Workload):
         }
         self.cand_per_particle = C / N
         self.nbr_per_particle = nn / N
+        # SURVEY.md §8(d) step roofline: 8 flops per stencil candidate per operator pass
+        self.survey = (sum(b for _, b, _ in self.kernels.values()),
+                       3 * 8.0 * C + (14 + 24 + 27) * nn,
+                       "3 passes x 8C + (14 + 24 + 27) n")
         import torch
         self.h_pos = torch.from_numpy(np.ascontiguousarray(sc.pos)).pin_memory()
         self.h_A = torch.from_numpy(np.ascontiguousarray(sc.fields["A"])).pin_memory()
@@ -332,6 +337,10 @@ class DamBreak(Workload):
         }
         self.cand_per_particle = C / N
         self.nbr_per_particle = nn / N
+        # SURVEY.md §8(d) step roofline: density 8C + 14n + 10, momentum 8C + 42n, integrator 20
+        self.survey = (sum(b for _, b, _ in self.kernels.values()),
+                       2 * 8.0 * C + (14 + 42) * nn + 30.0 * N,
+                       "2 passes x 8C + 56 n + 30 per particle")
         import torch
         self.h_r = torch.from_numpy(np.ascontiguousarray(sc.pos)).pin_memory()
         self.h_v = torch.zeros((d, sc.n), dtype=torch.float64).pin_memory()
@@ -441,6 +450,7 @@ class Gravity(Workload):
         N = float(sc.n)
         self.n_active = sc.n
         self.kernels = {107: ("all-pairs gravity", 56.0 * N, 20.0 * N * N)}
+        self.survey = (56.0 * N, 20.0 * N * N, "20 flops per pair")
         import torch
         self.h_r = torch.from_numpy(np.ascontiguousarray(sc.pos)).pin_memory()
         self.h_v = torch.from_numpy(np.ascontiguousarray(sc.fields["v"])).pin_memory()
@@ -496,6 +506,7 @@ class GravityShard(Gravity):
         self._forces()  # a(t = 0)
         self.n_active = nl
         self.kernels = {107: ("all-pairs gravity", 56.0 * nl, 20.0 * nl * N)}
+        self.survey = (56.0 * nl, 20.0 * nl * N, "20 flops per pair (this rank's bodies)")
         self.h_r = torch.from_numpy(np.ascontiguousarray(sc.pos[:, sl])).pin_memory()
         self.h_v = torch.from_numpy(np.ascontiguousarray(sc.fields["v"][:, sl])).pin_memory()
         self.h_out = {k: torch.empty((3, nl), dtype=torch.float64).pin_memory() for k in ("r", "v")}
@@ -591,6 +602,7 @@ class DamBreakSlab(DamBreak):
             301: ("symplectic integrator", (8.0 * (4 * d + 1) + 8 * 2 * d) * N, 20.0 * N),
             300: ("cell build", (8.0 * d + 8 + 60 + 4 + 16 * (3 * d + 5)) * N, 0.0),
         }
+        self.survey = None  # per-rank slabs: C and n are not counted
         self.cand_per_particle = float("nan")
         self.nbr_per_particle = float("nan")
         self.h_rows = torch.from_numpy(rows).pin_memory()
@@ -807,6 +819,14 @@ def run_ours(args, dist):
         "note": ("neighbour sums are FP64/latency-bound (SURVEY.md §8(d)); 'achieved' = "
                  "algorithmic bytes / mean CUDA-event launch time"),
     }
+    if wl.survey:  # the whole step against T* = max(B / BW_HBM, F / P_FP64), SURVEY.md §8(d)
+        Bs, Fs, basis = wl.survey
+        t_hbm = Bs / (peaks["hbm_gbs"] * 1e9) * 1e3
+        t_fp = Fs / (fp64_peak * 1e12) * 1e3
+        roofline["step"] = {"t_star_ms": round(max(t_hbm, t_fp), 4), "hbm_ms": round(t_hbm, 4),
+                            "fp64_ms": round(t_fp, 4),
+                            "frac": round(max(t_hbm, t_fp) / (ms_max / args.steps), 4),
+                            "flops": basis}
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "particle-updates/s",
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
