@@ -586,7 +586,10 @@ class DamBreakSlab(DamBreak):
         self.backend = slab.GpuBackend(ctx, p, self.FIELDS)
         dev = self.backend.device
         ex = slab.Exchanger(self.dist.pg, rank, world, periodic, dev)
-        self.rank_drv = slab.SlabRank(self.backend, ex, self.bounds, ncx, periodic)
+        # torch driver: re-balance the slab bounds every 100 steps
+        self.rank_drv = slab.SlabRank(self.backend, ex, self.bounds, ncx, periodic,
+                                      rebalance_every=0 if self.native else 100, x_lo=lo,
+                                      cell_size=cs)
         if self.native:
             uid = [nau.Context.comm_unique_id() if rank == 0 else None]
             if world > 1:
@@ -634,6 +637,7 @@ class DamBreakSlab(DamBreak):
         c.pop("neighbours_per_particle", None)
         c["slabs"] = self.bounds
         c["ghost_planes"] = 2
+        c["rebalance_every"] = self.rank_drv.rebalance_every
         c["exchange"] = "native NCCL (comm.cu)" if self.native else "torch.distributed (slab.py)"
         return c
 

@@ -31,8 +31,12 @@ import numpy as np
 
 def balanced_bounds(cell_x: np.ndarray, ncx: int, world: int) -> list[int]:
     """Slab bounds [b_0=0, ..., b_world=ncx] of whole x-cell planes with ~equal counts."""
-    hist = np.bincount(cell_x, minlength=ncx).astype(np.int64)
-    cum = np.cumsum(hist)
+    return bounds_from_hist(np.bincount(cell_x, minlength=ncx), ncx, world)
+
+
+def bounds_from_hist(hist: np.ndarray, ncx: int, world: int) -> list[int]:
+    """balanced_bounds from a per-plane particle-count histogram (length ncx)."""
+    cum = np.cumsum(np.asarray(hist, dtype=np.int64))
     total = cum[-1] if len(cum) else 0
     bounds = [0]
     for r in range(1, world):
@@ -59,6 +63,12 @@ class Exchanger:
         self.device = device
         self.left = (rank - 1) % world if (periodic or rank > 0) else None
         self.right = (rank + 1) % world if (periodic or rank < world - 1) else None
+
+    def allreduce_sum(self, t):
+        """Element-wise sum of a small int64 tensor over the ranks (in place)."""
+        if self.world > 1:
+            self.dist.all_reduce(t)
+        return t
 
     def swap(self, to_left, to_right, width):
         """Send row blocks to the neighbours; return (from_left, from_right).
@@ -118,12 +128,23 @@ class SlabRank:
 
     GHOST_PLANES = 2
 
-    def __init__(self, backend, exchanger, bounds, ncx, periodic):
+    def __init__(self, backend, exchanger, bounds, ncx, periodic, rebalance_every=0,
+                 x_lo=0.0, cell_size=None):
+        """rebalance_every > 0 (needs x_lo, cell_size: the x origin and size of the cell
+        planes) re-balances the slab bounds on the global x-plane histogram every that many
+        steps (the dam-break fluid moves right)."""
         self.b = backend
         self.x = exchanger
         self.r = exchanger.rank
+        self.bounds = list(bounds)
         self.lo_c, self.hi_c = bounds[self.r], bounds[self.r + 1]
         self.ncx, self.periodic = ncx, periodic
+        self.rebalance_every = rebalance_every
+        if rebalance_every and cell_size is None:
+            raise ValueError("rebalancing needs the x cell-plane geometry (x_lo, cell_size)")
+        self.x_lo, self.cs = x_lo, cell_size
+        self.steps = 0
+        self.rebalances = 0  # bound changes so far
 
     def _sel(self, c0, c1, ghost):
         """Rows with x-cell in [c0, c1) (wrapping on a ring)."""
@@ -153,6 +174,8 @@ class SlabRank:
         from_left, from_right = self.x.swap(to_left, to_right, self.b.width)
         owned = self.b.cat([keep, from_left, from_right])
         self.b.load(owned)
+        if self.rebalance_every and self.x.world > 1 and self.steps % self.rebalance_every == 0:
+            owned = self.rebalance(owned)
         gl = self._sel(self.lo_c, self.lo_c + g, 0)
         gr = self._sel(self.hi_c - g, self.hi_c, 0)
         if self.x.world == 1:
@@ -162,8 +185,51 @@ class SlabRank:
         ghosts = [self.b.mark_ghost(blk) for blk in (from_left, from_right) if blk is not None]
         self.b.load(self.b.cat([owned] + ghosts))
 
+    def plane_hist(self, rows):
+        """Global per-x-plane count of owned particles (cell_x_of on the rows' x column)."""
+        import torch
+        x = rows[:, 0]
+        c = torch.floor((x - self.x_lo) / self.cs).to(torch.int64)
+        c = torch.remainder(c, self.ncx) if self.periodic else c.clamp(0, self.ncx - 1)
+        h = torch.bincount(c, minlength=self.ncx)
+        return self.x.allreduce_sum(h.to(torch.int64)).cpu().numpy()
+
+    def rebalance(self, owned):
+        """New bounds from the global plane histogram; owned particles then hop rank by rank
+        toward their new owner (a bound may move past a whole neighbouring slab). The local
+        set holds owned particles only (ghosts are refreshed by the caller); every particle
+        keeps its global id, so sums stay in the single-GPU order."""
+        import torch
+        new = bounds_from_hist(self.plane_hist(owned), self.ncx, self.x.world)
+        if new == self.bounds:
+            return owned
+        self.bounds = new
+        self.lo_c, self.hi_c = new[self.r], new[self.r + 1]
+        self.rebalances += 1
+        lo, hi, n = self.lo_c, self.hi_c, self.ncx
+        if self.periodic:
+            out = n - (hi - lo)          # planes outside the slab, hi .. lo-1 around the ring
+            right = (out + 1) // 2       # the nearer half goes right, the rest left
+            rng_r, rng_l = (hi, hi + right), (hi + right, hi + out)
+        else:
+            rng_r, rng_l = (hi, n), (0, lo)
+        for _ in range(self.x.world + 1):
+            to_right = self._sel(*rng_r, 0)
+            to_left = self._sel(*rng_l, 0)
+            cnt = sum(0 if t is None else int(t.shape[0]) for t in (to_left, to_right))
+            pending = self.x.allreduce_sum(torch.tensor([cnt], dtype=torch.int64,
+                                                        device=self.x.device))
+            if int(pending.item()) == 0:
+                return owned
+            keep = self.b.select(lo, hi, 0)
+            from_left, from_right = self.x.swap(to_left, to_right, self.b.width)
+            owned = self.b.cat([keep, from_left, from_right])
+            self.b.load(owned)
+        raise RuntimeError("slab rebalance: particles still misplaced after world+1 hops")
+
     def step(self):
         self.b.step()
+        self.steps += 1
         self.exchange()
 
 

@@ -51,7 +51,7 @@ def make_scene(kind):
     return sc, True
 
 
-def run_rank(rank, world, port_, kind, out):
+def run_rank(rank, world, port_, kind, out, rebalance=0, skew=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port_)
     if world > 1:
@@ -61,27 +61,30 @@ def run_rank(rank, world, port_, kind, out):
     lo, cs = sc.min_cells[0] * sc.cell_size[0], sc.cell_size[0]
     cx = slab.cell_x_of(sc.pos[0], lo, cs, ncx, periodic)
     bounds = slab.balanced_bounds(cx, ncx, world)
+    if skew:  # badly balanced start: every slab but the last two planes wide
+        bounds = [2 * i for i in range(world)] + [ncx]
     be = slab_oracle.OracleBackend(sc, ncx, periodic)
     ex = slab.Exchanger(dist if world > 1 else None, rank, world, periodic, "cpu")
-    r = slab.SlabRank(be, ex, bounds, ncx, periodic)
+    r = slab.SlabRank(be, ex, bounds, ncx, periodic, rebalance_every=rebalance, x_lo=lo,
+                      cell_size=cs)
     be.load(torch.from_numpy(slab.initial_rows(sc, slab_oracle.FIELDS, bounds, rank, ncx, periodic)))
     for _ in range(STEPS):
         r.step()
     owned = be.rows[(be.rows[:, be.col_ghost] == 0) & be.active]
     first = set(slab.initial_rows(sc, slab_oracle.FIELDS, bounds, rank, ncx, periodic)[:, -2].tolist())
-    out[rank] = (owned, len(set(owned[:, -2].tolist()) ^ first))
+    out[rank] = (owned, len(set(owned[:, -2].tolist()) ^ first), r.rebalances, r.bounds)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def _worker(rank, world, port_, kind, q):
+def _worker(rank, world, port_, kind, q, rebalance, skew):
     out = {}
-    run_rank(rank, world, port_, kind, out)
+    run_rank(rank, world, port_, kind, out, rebalance, skew)
     q.put((rank, out[rank]))
 
 
-def run_world(world, kind):
+def run_world(world, kind, rebalance=0, skew=False, info=None):
     if world == 1:
         out = {}
         run_rank(0, 1, 0, kind, out)
@@ -89,7 +92,8 @@ def run_world(world, kind):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port_ = free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port_, kind, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port_, kind, q, rebalance, skew))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(world))
@@ -97,6 +101,8 @@ def run_world(world, kind):
         p.join(timeout=60)
         assert p.exitcode == 0
     moved = sum(res[r][1] for r in range(world))
+    if info is not None:
+        info.extend(res[r][2:] for r in range(world))
     return np.concatenate([res[r][0] for r in range(world)], axis=0), moved
 
 
@@ -111,6 +117,31 @@ def test_two_slabs_match_one_rank_bitwise(kind):
     assert len(np.unique(two[:, gid])) == len(two), "a particle is owned twice"
     np.testing.assert_array_equal(two[:, gid], one[:, gid])  # no particle lost
     np.testing.assert_array_equal(two, one)
+
+
+@pytest.mark.parametrize("kind,world", [("dam", 3), ("periodic", 3)])
+def test_rebalanced_slabs_match_one_rank_bitwise(kind, world):
+    """SURVEY.md §8(e) re-balancing: start from skewed bounds (two-plane slabs and one
+    huge one), re-balance every 4 steps on the global plane histogram; bounds move by
+    more than a whole slab, so particles hop over a rank, and results stay bitwise."""
+    one, _ = run_world(1, kind)
+    info = []
+    many, _ = run_world(world, kind, rebalance=4, skew=True, info=info)
+    assert all(n >= 1 for n, _ in info), "bounds never changed"
+    assert len({tuple(b) for _, b in info}) == 1, "ranks disagree on the bounds"
+    final = info[0][1]
+    assert final != [0, 2, 4, final[-1]] and all(final[i + 1] - final[i] >= 2 for i in range(world))
+    gid = one.shape[1] - 2
+    one = one[np.argsort(one[:, gid])]
+    many = many[np.argsort(many[:, gid])]
+    assert len(np.unique(many[:, gid])) == len(many), "a particle is owned twice"
+    np.testing.assert_array_equal(many, one)
+
+
+def test_bounds_from_hist():
+    h = np.array([0, 0, 5, 50, 50, 50, 50, 5, 0, 0])
+    cx = np.repeat(np.arange(10), h)
+    assert slab.bounds_from_hist(h, 10, 3) == slab.balanced_bounds(cx, 10, 3)
 
 
 def test_balanced_bounds():
