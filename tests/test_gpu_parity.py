@@ -710,6 +710,128 @@ def test_slab_path_single_rank_matches_plain(ctx):
     ctx2.close()
 
 
+class _Hub:
+    """In-process rendezvous for slab ranks run as host threads on one GPU: each rank has
+    its own context and stream; rows meet on the host side (no kernel waits on another
+    rank's kernel), so the multi-rank SlabRank logic runs on the real CUDA backend."""
+
+    def __init__(self, world):
+        import threading
+        self.world, self.bar, self.box = world, threading.Barrier(world, timeout=120), {}
+
+
+class _ThreadExchanger:
+    """slab.Exchanger's contract (swap / allreduce_sum) over a _Hub."""
+
+    def __init__(self, hub, rank, periodic, device):
+        w = hub.world
+        self.hub, self.rank, self.world, self.periodic, self.device = hub, rank, w, periodic, device
+        self.left = (rank - 1) % w if (periodic or rank > 0) else None
+        self.right = (rank + 1) % w if (periodic or rank < w - 1) else None
+
+    def swap(self, to_left, to_right, width):
+        import torch
+        h = self.hub
+        torch.cuda.synchronize()  # blocks come from other contexts' streams
+        h.box[(self.rank, "L")] = to_left
+        h.box[(self.rank, "R")] = to_right
+        h.bar.wait()
+        empty = torch.empty((0, width), dtype=torch.float64, device=self.device)
+
+        def take(src, side):
+            if src is None:
+                return None
+            t = h.box.get((src, side))
+            return empty if t is None else t.clone()
+        fl, fr = take(self.left, "R"), take(self.right, "L")
+        torch.cuda.synchronize()
+        h.bar.wait()
+        return fl, fr
+
+    def allreduce_sum(self, t):
+        h = self.hub
+        h.box[(self.rank, "sum")] = t.clone()
+        h.bar.wait()
+        tot = sum(h.box[(r, "sum")].cpu() for r in range(self.world))
+        h.bar.wait()
+        t.copy_(tot.to(t.device))
+        return t
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_ranks_with_rebalancing_match_plain(ctx, world):
+    """SURVEY.md §8(e) on the CUDA backend: `world` slab ranks (threads, one context each,
+    one GPU) from skewed bounds with migration, ghost refresh and re-balancing every 3
+    steps; owned particles gathered by global id = the single-context path, bitwise."""
+    import threading
+
+    import bench
+    from paper_1710_08259_b200 import slab as slab_mod
+
+    def scene():
+        sc = scenes.dam_break(2, dx=0.05, fluid=(1.0, 1.0), tank=(2.0, 1.6))
+        sc.fields["v"][0, : sc.params["n_fluid"]] = 6.0
+        return sc
+
+    steps = 9
+    plain = bench.DamBreak(2)
+    plain.sc = scene()
+    ctx.set_mode(False)
+    plain.setup(ctx)
+    for _ in range(steps):
+        plain.step(ctx)
+    ref_r, ref_v = ctx.download("r"), ctx.download("v")
+    hub = _Hub(world)
+    out, errs, drv = {}, [], {}
+
+    def rank_main(rank):
+        try:
+            class D:
+                pg = None
+            D.world, D.rank, D.local = world, rank, 0
+            c = nau.Context(0)
+            sl = bench.DamBreakSlab(2, D())
+            sl.sc = scene()
+            sl.setup(c)
+            sc = sl.sc
+            ncx = sc.max_cells[0] - sc.min_cells[0]
+            # skewed start (two-plane slabs, one huge): re-balancing must move bounds
+            # past whole slabs, so particles hop over a rank
+            skew = [2 * i for i in range(world)] + [ncx]
+            import torch
+            rows = slab_mod.initial_rows(sc, sl.FIELDS, skew, rank, ncx, False)
+            sl.backend.load(torch.from_numpy(rows).to(sl.backend.device))
+            ex = _ThreadExchanger(hub, rank, False, sl.backend.device)
+            r = slab_mod.SlabRank(sl.backend, ex, skew, ncx, False, rebalance_every=3,
+                                  x_lo=sc.min_cells[0] * sc.cell_size[0],
+                                  cell_size=sc.cell_size[0])
+            drv[rank] = r
+            for _ in range(steps):
+                r.step()
+            own = c.download("ghost")[0] == 0
+            out[rank] = (c.download("gid")[0][own].astype(int), c.download("r")[:, own],
+                         c.download("v")[:, own])
+            c.close()
+        except BaseException as e:  # surface thread failures in the test
+            errs.append(e)
+            hub.bar.abort()
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    assert all(drv[r].rebalances >= 1 for r in range(world)), "bounds never changed"
+    gid = np.concatenate([out[r][0] for r in range(world)])
+    assert np.array_equal(np.sort(gid), np.arange(ref_r.shape[1])), "a particle lost or owned twice"
+    r2, v2 = np.empty_like(ref_r), np.empty_like(ref_v)
+    for r in range(world):
+        r2[:, out[r][0]], v2[:, out[r][0]] = out[r][1], out[r][2]
+    np.testing.assert_array_equal(r2, ref_r)
+    np.testing.assert_array_equal(v2, ref_v)
+
+
 def test_native_slab_exchange_single_rank_matches_plain(ctx):
     """nau_comm_init / nau_migrate / nau_halo_exchange (comm.cu, NCCL bound at run
     time) on one rank: the step loop through the native exchange = the plain path,
