@@ -251,13 +251,15 @@ class Microbench(Workload):
             100: ("sph_S density", 32.0 * N + 4.0 * nn, 14 * nn),
             102: ("sph_G11 gradient", 64.0 * N + 4.0 * nn, 24 * nn),
             103: ("sph_L0 Laplacian", 48.0 * N + 4.0 * nn, 27 * nn),
+            # fused G11 + L0 (one list walk): x, A, rho in; G, L out; A, m, rho at j
+            110: ("sph_G11+L0 fused", 80.0 * N + 4.0 * nn, (24 + 27) * nn),
             302: ("neighbour-list build", 20.0 * N + 4.0 * nn, 0.0),
             300: ("cell build", (32.0 + 60.0 + 4.0 + 16.0 * 8) * N, 0.0),
         }
         self.cand_per_particle = C / N
         self.nbr_per_particle = nn / N
         # SURVEY.md §8(d) step roofline: 8 flops per stencil candidate per operator pass
-        self.survey = (sum(b for _, b, _ in self.kernels.values()),
+        self.survey = (sum(b for k, (_, b, _) in self.kernels.items() if k != 110),
                        3 * 8.0 * C + (14 + 24 + 27) * nn,
                        "3 passes x 8C + (14 + 24 + 27) n")
         import torch
@@ -271,8 +273,9 @@ class Microbench(Workload):
         prm = self.sc.params
         ctx.build_cells()
         ctx.interact("sph_S", [1.0, prm["mass"], 1.0, prm["radius"]], "rho", kernel=self.kw)
-        ctx.interact("sph_G11", ["A", prm["mass"], "rho", prm["radius"]], "G", kernel=self.kw)
-        ctx.interact("sph_L0", ["A", prm["mass"], "rho", prm["radius"]], "L", kernel=self.kw)
+        # G = sph_G11(A, m, rho), L = sph_L0(A, m, rho): one fused list walk (FAST mode;
+        # the two interact() calls otherwise), bitwise equal to the two calls
+        ctx.interact_g11_l0(["A", prm["mass"], "rho", prm["radius"]], "G", "L", kernel=self.kw)
 
     def e2e_step(self, ctx):
         ctx.upload_async("r", self.h_pos.data_ptr())

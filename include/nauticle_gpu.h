@@ -183,6 +183,15 @@ typedef struct {
 nau_status nau_interact(nau_ctx* ctx, int op, int kernel_family, int kernel_dim,
                         const nau_operand* ops, int n_ops, int out_field);
 
+/* Two consecutive equations  out_g = sph_G11(A, m, rho, K, R);  out_l = sph_L0(A, m,
+ * rho, K, R)  (interactions.cpp:81-126, evaluated in listed order by Case::solve_step,
+ * case.cpp:9-67). Neither reads the other's output, so in FAST mode one walk of the
+ * neighbour list evaluates both sums (one gather per neighbour); results, errors and
+ * warnings equal the two nau_interact calls. Any other case (EXACT mode, an output
+ * aliasing an operand, bad shapes) runs exactly those two calls. */
+nau_status nau_interact_g11_l0(nau_ctx* ctx, int kernel_family, int kernel_dim,
+                               const nau_operand* ops, int n_ops, int out_g, int out_l);
+
 /* ≙ EulerNode (sfl/ast.cpp:180-191): out = x + xdot*dt on active particles. */
 nau_status nau_euler(nau_ctx* ctx, int x, int xdot, double dt, int out_field);
 

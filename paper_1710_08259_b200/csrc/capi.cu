@@ -849,6 +849,44 @@ nau_status nau_interact(nau_ctx* c, int op, int kf, int kdim, const nau_operand*
     return NAU_OK;
 }
 
+nau_status nau_interact_g11_l0(nau_ctx* c, int kf, int kdim, const nau_operand* ops, int nops,
+                               int out_g, int out_l) {
+    // Fused only where it is observably the same as the two calls in sequence: FAST
+    // mode, valid shapes, and neither output aliasing an operand or the other output
+    // (sph_L0 then reads exactly what sph_G11 read). Otherwise: the two calls, which
+    // also produce the reference's error messages.
+    const int dim = c->dom.dim;
+    bool fuse = c->mode == NAU_MODE_FAST && nops == 4 && ops != nullptr && out_g != out_l &&
+                field_ok(c, out_g) && field_ok(c, out_l) && out_g != 0 && out_l != 0;
+    for (int k = 0; fuse && k < nops; ++k) {
+        const int f = ops[k].field_id;
+        fuse = f != out_g && f != out_l && (f < 0 || field_ok(c, f));
+    }
+    if (fuse) {
+        const int f = ops[0].field_id;
+        const int ar = f >= 0 ? c->fields[f].rows : ops[0].rows;
+        const int acl = f >= 0 ? c->fields[f].cols : ops[0].cols;
+        fuse = ar == 1 && acl == 1 && c->fields[out_g].rows == dim && c->fields[out_g].cols == 1 &&
+               c->fields[out_l].rows == 1 && c->fields[out_l].cols == 1;
+    }
+    if (!fuse) {
+        nau_status s = nau_interact(c, NAU_OP_SPH_G11, kf, kdim, ops, nops, out_g);
+        if (s != NAU_OK) return s;
+        return nau_interact(c, NAU_OP_SPH_L0, kf, kdim, ops, nops, out_l);
+    }
+    if (c->dirty || !c->built_once) {
+        nau_status s = nau_build_cells(c);  // case.cpp:11
+        if (s != NAU_OK) return s;
+    }
+    nau::Opd d_ops[4];
+    for (int k = 0; k < 4; ++k) d_ops[k] = nau::make_opd(c, ops[k]);
+    bool lists = false;
+    if (ops[3].field_id < 0 && ops[3].value[0] > 0.0)
+        lists = nau::nlist_for(c, ops[3].value[0], false);
+    nau::launch_g11_l0_fast(c, kf, kdim, d_ops, c->fields[out_g].d, c->fields[out_l].d, lists);
+    return NAU_OK;
+}
+
 nau_status nau_euler(nau_ctx* c, int x, int xdot, double dt, int out_field) {
     if (!field_ok(c, x) || !field_ok(c, xdot) || !field_ok(c, out_field))
         return fail(c, NAU_ERR_ARG, "bad field id");

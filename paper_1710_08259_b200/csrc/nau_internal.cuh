@@ -452,6 +452,8 @@ void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p, bool lists);
 void launch_reduce(nau_ctx* c, int kind, const double* f, int comps, double* h_out);
 // fast.cu
 bool fast_supports(int op, int a_rows, int a_cols, int dim);
+void launch_g11_l0_fast(nau_ctx* c, int kf, int kdim, const Opd* ops, double* out_g,
+                        double* out_l, bool lists);
 void launch_interact_fast(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, double* out,
                           int a_rows, bool lists = false);
 void launch_wcsph_fast(nau_ctx* c, const nau_wcsph_params* p, double4* vp, int lists);

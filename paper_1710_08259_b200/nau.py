@@ -35,7 +35,7 @@ EXPORTS = [
     "nau_active_count", "nau_get_active", "nau_alloc_field", "nau_free_field", "nau_upload",
     "nau_download", "nau_fill", "nau_copy_field", "nau_field_device_ptr", "nau_boundary_shift",
     "nau_build_cells", "nau_cells_dirty", "nau_rebuild_count", "nau_warning_count", "nau_ncells",
-    "nau_cell_tables", "nau_neighbor_counts", "nau_interact", "nau_euler", "nau_symplectic_step",
+    "nau_cell_tables", "nau_neighbor_counts", "nau_interact", "nau_interact_g11_l0", "nau_euler", "nau_symplectic_step",
     "nau_wcsph_step", "nau_reduce", "nau_sync", "nau_last_error", "nau_profile_enable",
     "nau_profile_ms", "nau_launch_count", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
     "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows", "nau_dem_step",
@@ -133,6 +133,7 @@ def load():
         "nau_cell_tables": (i, [vp, vp, vp, vp, vp]),
         "nau_neighbor_counts": (i, [vp, d, vp]),
         "nau_interact": (i, [vp, i, i, i, C.POINTER(Operand), i, i]),
+        "nau_interact_g11_l0": (i, [vp, i, i, C.POINTER(Operand), i, i, i]),
         "nau_euler": (i, [vp, i, i, d, i]),
         "nau_symplectic_step": (i, [vp, i, i, i, d]),
         "nau_wcsph_step": (i, [vp, C.POINTER(WcsphParams)]),
@@ -563,6 +564,14 @@ class Context:
         kf, kd = (K_WENDLAND, self.dim) if kernel is None else decode_kernel(kernel)
         arr = (Operand * len(operands))(*[self._operand(o) for o in operands])
         self._check(self.L.nau_interact(self.h, op, kf, kd, arr, len(operands), self._fid(out)))
+
+    def interact_g11_l0(self, operands, out_g, out_l, kernel=None):
+        """out_g = sph_G11(operands); out_l = sph_L0(operands), in that order — one fused
+        list walk in FAST mode (nau_interact_g11_l0), else the two interact() calls."""
+        kf, kd = (K_WENDLAND, self.dim) if kernel is None else decode_kernel(kernel)
+        arr = (Operand * len(operands))(*[self._operand(o) for o in operands])
+        self._check(self.L.nau_interact_g11_l0(self.h, kf, kd, arr, len(operands),
+                                               self._fid(out_g), self._fid(out_l)))
 
     def euler(self, x, xdot, dt, out):
         self._check(self.L.nau_euler(self.h, self._fid(x), self._fid(xdot), float(dt),

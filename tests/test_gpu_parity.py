@@ -406,6 +406,105 @@ def test_fast_mode_microbench_full_size(ctx):
         assert rel_err(out[True][k], out[False][k]) <= TOL_STEP, k
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_fused_g11_l0_equals_two_calls(seed):
+    """nau_interact_g11_l0 (one list walk for sph_G11 + sph_L0) = the two nau_interact
+    calls bitwise, FAST and EXACT, incl. image/mirror domains, coincident-particle
+    warnings and aliasing fall-backs."""
+    rng = np.random.default_rng(900 + seed)
+    spec = cases.random_spec(rng, dim=int(rng.integers(2, 4)), n=int(rng.integers(300, 3000)))
+    if seed % 2:  # coincident distinct particles: sph_L0 warns, sph_G11 skips
+        spec["pos"][:, 1] = spec["pos"][:, 0]
+    dim = spec["dim"]
+    m, R = float(spec["consts"]["m"]), float(spec["consts"]["R"])
+    for kw in (f"Wp5{dim}220", f"Wc3{dim}220"):
+        for fast in (True, False):
+            for ops in (["A", m, "rho", R], ["A", "M", "rho", R]):
+                res = []
+                for fused in (False, True):
+                    c = cases.gpu_context(spec)
+                    c.set_mode(fast)
+                    c.add_field("G", dim, 1, 0.0)
+                    c.add_field("L", 1, 1, 0.0)
+                    w0 = c.warning_count
+                    if fused:
+                        c.interact_g11_l0(ops, "G", "L", kernel=kw)
+                    else:
+                        c.interact("sph_G11", ops, "G", kernel=kw)
+                        c.interact("sph_L0", ops, "L", kernel=kw)
+                    c.sync()
+                    res.append((c.download("G"), c.download("L"), c.warning_count - w0))
+                    c.close()
+                np.testing.assert_array_equal(res[1][0], res[0][0])
+                np.testing.assert_array_equal(res[1][1], res[0][1])
+                assert res[1][2] == res[0][2]
+                if seed % 2:
+                    assert res[0][2] > 0
+
+
+def test_fused_g11_l0_microbench_full_size(ctx):
+    """cfg1 at full size: the fused pass equals sph_G11 then sph_L0 bitwise (FAST)."""
+    sc = scenes.sph_microbench()
+    prm = sc.params
+    ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+    ctx.set_particles(sc.pos)
+    ctx.add_field("A", 1, 1, sc.fields["A"])
+    for f, r in (("rho", 1), ("G", 3), ("L", 1)):
+        ctx.add_field(f, r, 1, 0.0)
+    ctx.boundary_shift()
+    ctx.set_mode(True)
+    ops = ["A", prm["mass"], "rho", prm["radius"]]
+    ctx.interact("sph_S", [1.0, prm["mass"], 1.0, prm["radius"]], "rho", kernel="Wc33220")
+    ctx.interact("sph_G11", ops, "G", kernel="Wc33220")
+    ctx.interact("sph_L0", ops, "L", kernel="Wc33220")
+    ref = ctx.download("G"), ctx.download("L")
+    ctx.fill("G", 0.0)
+    ctx.fill("L", 0.0)
+    ctx.interact_g11_l0(ops, "G", "L", kernel="Wc33220")
+    ctx.set_mode(False)
+    np.testing.assert_array_equal(ctx.download("G"), ref[0])
+    np.testing.assert_array_equal(ctx.download("L"), ref[1])
+
+
+def test_fused_g11_l0_errors_like_two_calls():
+    """rho_j == 0 / rho_i == 0: same error (message, particle) as the two calls; an
+    output aliasing an operand takes the two-call path."""
+    rng = np.random.default_rng(77)
+    spec = cases.random_spec(rng, dim=3, n=800)
+    spec["fields"]["rho"][0, 123] = 0.0
+    msgs = []
+    for fused in (False, True):
+        c = cases.gpu_context(spec)
+        c.set_mode(True)
+        c.add_field("G", 3, 1, 0.0)
+        c.add_field("L", 1, 1, 0.0)
+        with pytest.raises(nau.NauError) as ei:
+            if fused:
+                c.interact_g11_l0(["A", 0.5, "rho", 0.3], "G", "L", kernel="Wp53220")
+            else:
+                c.interact("sph_G11", ["A", 0.5, "rho", 0.3], "G", kernel="Wp53220")
+                c.interact("sph_L0", ["A", 0.5, "rho", 0.3], "L", kernel="Wp53220")
+            c.sync()
+        msgs.append(str(ei.value))
+        c.close()
+    assert msgs[0] == msgs[1] and msgs[0]
+    spec["fields"]["rho"][0, 123] = 1000.0
+    outs = []
+    for fused in (False, True):
+        c = cases.gpu_context(spec)
+        c.set_mode(True)
+        c.add_field("G", 3, 1, 0.0)
+        if fused:
+            c.interact_g11_l0(["A", 0.5, "rho", 0.3], "G", "A", kernel="Wp53220")
+        else:
+            c.interact("sph_G11", ["A", 0.5, "rho", 0.3], "G", kernel="Wp53220")
+            c.interact("sph_L0", ["A", 0.5, "rho", 0.3], "A", kernel="Wp53220")
+        outs.append((c.download("G"), c.download("A")))
+        c.close()
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+
+
 def test_fast_mode_dam_break_vs_port(ctx):
     """cfg0 deck in FAST mode: 1 step within 1e-10, 10 steps within 1e-6 of the oracle."""
     sc = scenes.dam_break(2)
