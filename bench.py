@@ -173,11 +173,12 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of each hot kernel from the committed ncu capture."""
+def ncu_traffic(config):
+    """Per-launch DRAM bytes of each hot kernel of BASELINE config `config` from the
+    committed ncu capture (profiles/traffic.json, keyed "cfg<k>"; {} if not captured)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f)
+            return json.load(f).get(f"cfg{config}", {})
     except OSError:
         return {}
 
@@ -799,7 +800,7 @@ def run_ours(args, dist):
     # ---- roofline of the dominant kernel ----
     peaks, peak_kind = measured_peaks()
     fp64_peak = nau.fp64_peak_tflops(dist.local)
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(args.config if args.mode == "fast" else f"{args.config}_exact")
     per_kernel = {}
     for cls, (label, B, F) in wl.kernels.items():
         tot, cnt = prof[cls]

@@ -27,8 +27,15 @@ echo "full2 rc=$?"
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
   --master-port 29517 bench.py --gpus 1 --steps 3 --warmup 3 --slab --no-cpu-baseline > gpurun_out/${T}_slab_cfg2.json 2> gpurun_out/${T}_slab_cfg2.err
 echo "slab rc=$?"; tail -c 400 gpurun_out/${T}_slab_cfg2.json
+timeout 600 python tools/profile_step.py --config 1 --steps 1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/${T}_launches_cfg1.csv python tools/profile_step.py --config 1 --steps 1 > gpurun_out/${T}_ncu_launch1.log 2>&1
+echo "launches1 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sph_fast -c 2 \
+  -o /tmp/${T}_full_cfg1 python tools/profile_step.py --config 1 --steps 1 > gpurun_out/${T}_ncu_full1.log 2>&1
+echo "full1 rc=$?"
 # reports stay on the box (gpurun returns <= 64 MiB): summaries + raw metric pages come back
-for k in cfg2 cfg4; do
+for k in cfg1 cfg2 cfg4; do
   python tools/summarize_ncu.py full /tmp/${T}_full_$k.ncu-rep > gpurun_out/${T}_ncu_full_$k.md 2>/dev/null
   ncu -i /tmp/${T}_full_$k.ncu-rep --page raw --csv > gpurun_out/${T}_ncu_raw_$k.csv 2>/dev/null
 done
