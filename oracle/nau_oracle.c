@@ -9,6 +9,10 @@
 
 #include <math.h>
 #include <stdlib.h>
+#include <limits.h>
+#include <pthread.h>
+#include <stdatomic.h>
+#include <unistd.h>
 #include <string.h>
 
 static const double kPi = 3.14159265358979323846;
@@ -143,6 +147,55 @@ static void push(cand_buf* b, int j, const double* rel, const double* guide) {
     }
 }
 
+
+/* ---- host threads: a dynamic parallel-for over particles (the role of
+ * ThreadPool::parallel_blocks, thread_pool.hpp:20-46; particles are independent) ---- */
+typedef void (*nor_body_fn)(void* arg, int i, cand_buf* b);
+typedef struct {
+    nor_body_fn fn;
+    void* arg;
+    int n, chunk;
+    atomic_int next;
+} nor_pfor;
+
+static void* pfor_worker(void* p) {
+    nor_pfor* t = (nor_pfor*)p;
+    cand_buf b = {0, 0, 0};
+    for (;;) {
+        int s = atomic_fetch_add(&t->next, t->chunk);
+        if (s >= t->n) break;
+        int e = s + t->chunk < t->n ? s + t->chunk : t->n;
+        for (int i = s; i < e; ++i) t->fn(t->arg, i, &b);
+    }
+    free(b.c);
+    return NULL;
+}
+
+static int nor_threads(void) {
+    const char* e = getenv("NOR_THREADS");
+    long t = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+    return t < 1 ? 1 : (t > 256 ? 256 : (int)t);
+}
+
+static void parallel_for(int n, int chunk, nor_body_fn fn, void* arg) {
+    nor_pfor t;
+    t.fn = fn;
+    t.arg = arg;
+    t.n = n;
+    t.chunk = chunk;
+    atomic_init(&t.next, 0);
+    int nt = nor_threads();
+    if ((long)nt * chunk > n) nt = (n + chunk - 1) / chunk;
+    if (nt <= 1) {
+        pfor_worker(&t);
+        return;
+    }
+    pthread_t th[256];
+    for (int k = 1; k < nt; ++k) pthread_create(&th[k], NULL, pfor_worker, &t);
+    pfor_worker(&t);
+    for (int k = 1; k < nt; ++k) pthread_join(th[k], NULL);
+}
+
 static void candidates(const nor_ps* ps, int i, cand_buf* out) {
     out->n = 0;
     if (!ps->active[i]) return;
@@ -243,16 +296,24 @@ static double norm_d(const double* v, int d) {
     return sqrt(s);
 }
 
+typedef struct {
+    nor_ps* ps;
+    double radius;
+    int* counts;
+} nc_arg;
+
+static void nc_body(void* p, int i, cand_buf* b) {
+    nc_arg* a = (nc_arg*)p;
+    candidates(a->ps, i, b);
+    int c = 0;
+    for (int k = 0; k < b->n; ++k)
+        if (norm_d(b->c[k].rel, a->ps->dom.dim) <= a->radius) ++c;
+    a->counts[i] = c;
+}
+
 void nor_neighbor_counts(nor_ps* ps, double radius, int* counts) {
-    cand_buf b = {0, 0, 0};
-    for (int i = 0; i < ps->n; ++i) {
-        candidates(ps, i, &b);
-        int c = 0;
-        for (int k = 0; k < b.n; ++k)
-            if (norm_d(b.c[k].rel, ps->dom.dim) <= radius) ++c;
-        counts[i] = c;
-    }
-    free(b.c);
+    nc_arg a = {ps, radius, counts};
+    parallel_for(ps->n, 256, nc_body, &a);
 }
 
 /* ---- smoothing kernels: src/kernel.cpp:37-69 (Wendland); cubic spline is new ---- */
@@ -345,10 +406,10 @@ static int any_reflected(const double* guide, int d) {
 }
 
 /* interactions.cpp:32-38 */
-static void warn_coincident(nor_ps* ps, int i, int j, const double* guide) {
+static void warn_coincident(const nor_ps* ps, int i, int j, const double* guide, long* warns) {
     if (i == j) return;
     if (any_reflected(guide, ps->dom.dim)) return;
-    ps->warnings++;
+    ++*warns;
 }
 
 /* interactions.cpp:288-316 (Hertz) and the restated linear spring-dashpot law. */
@@ -399,16 +460,17 @@ static void contact_force(int law, double Ri, double Rj, double Pi, double Pj, d
     }
 }
 
-int nor_interact(int op, int kfamily, int kdim, nor_ps* ps, const nor_operand* ops, int nops,
-                 double* out, int out_comps, long* bad) {
+/* One particle i of InteractionOp::eval (interactions.cpp:40-316). Returns 0 and the
+ * result in out[c*n + i], or 1 with the offending index in *bad. Coincident-pair and
+ * at-goal warnings are added to *warns. `b` is a per-thread candidate buffer. */
+static int interact_one(int op, int kfamily, int kdim, const nor_ps* ps, const nor_operand* ops,
+                        int nops, double* out, int out_comps, int i, cand_buf* bp, long* warns,
+                        long* bad) {
     const int n = ps->n;
     const int d = ps->dom.dim;
-    cand_buf b = {0, 0, 0};
+    cand_buf b = *bp;
     int rc = 0;
-    *bad = -1;
-    (void)nops;
-    for (int i = 0; i < n && rc == 0; ++i) {
-        if (!ps->active[i]) continue;
+    do {
         double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         if (op == NOR_GRAVITY) { /* interactions.cpp:195-214 */
             double G = opv(&ops[1], n, 0, i);
@@ -515,7 +577,7 @@ int nor_interact(int op, int kfamily, int kdim, nor_ps* ps, const nor_operand* o
                     case NOR_SPH_L0: { /* interactions.cpp:104-126 */
                         if (dist > radius) break;
                         if (dist <= 0.0) {
-                            warn_coincident(ps, i, j, cd->guide);
+                            warn_coincident(ps, i, j, cd->guide, warns);
                             break;
                         }
                         double rho_j = opv(&ops[2], n, 0, j);
@@ -535,7 +597,7 @@ int nor_interact(int op, int kfamily, int kdim, nor_ps* ps, const nor_operand* o
                     case NOR_SPH_A: { /* interactions.cpp:128-150 */
                         if (dist > radius) break;
                         if (dist <= 0.0) {
-                            warn_coincident(ps, i, j, cd->guide);
+                            warn_coincident(ps, i, j, cd->guide, warns);
                             break;
                         }
                         double v_j[9];
@@ -577,7 +639,7 @@ int nor_interact(int op, int kfamily, int kdim, nor_ps* ps, const nor_operand* o
                 const double s = v0 / e0n;
                 for (int a = 0; a < d; ++a) drv[a] = (e0[a] * s - v_i[a]) / tau;
             } else {
-                ps->warnings++; /* agent already at its desired position */
+                ++*warns; /* agent already at its desired position */
             }
             double cs_min = ps->dom.cs[0];
             for (int a = 1; a < d; ++a) cs_min = ps->dom.cs[a] < cs_min ? ps->dom.cs[a] : cs_min;
@@ -620,7 +682,7 @@ int nor_interact(int op, int kfamily, int kdim, nor_ps* ps, const nor_operand* o
                 if (dist > radius) continue;
                 if (images_only && !any_reflected(cd->guide, d)) continue;
                 if (dist <= 0.0) {
-                    if (law == NOR_DEM_HERTZ) warn_coincident(ps, i, j, cd->guide);
+                    if (law == NOR_DEM_HERTZ) warn_coincident(ps, i, j, cd->guide, warns);
                     continue;
                 }
                 double Rj = opv(&ops[1], n, 0, j);
@@ -645,9 +707,70 @@ int nor_interact(int op, int kfamily, int kdim, nor_ps* ps, const nor_operand* o
                 for (int a = 0; a < d; ++a) acc[a] = acc[a] / mi;
             for (int c = 0; c < out_comps; ++c) out[(long)c * n + i] = acc[c];
         }
-    }
-    free(b.c);
+    } while (0);
+    *bp = b;
     return rc;
+}
+
+/* The per-equation loop of Case::solve_equation (case.cpp:31-54) over host threads
+ * (ThreadPool::parallel_blocks, thread_pool.hpp:20-46, also evaluates particles
+ * independently). Serial semantics are kept: the reported error is the one of the
+ * lowest failing particle, and warnings count up to and including that particle. */
+typedef struct {
+    int op, kfamily, kdim, nops, out_comps;
+    const nor_ps* ps;
+    const nor_operand* ops;
+    double* out;
+    long* warns;
+    pthread_mutex_t mu;
+    long first_fail, fail_bad;
+} ia_arg;
+
+static void ia_body(void* p, int i, cand_buf* b) {
+    ia_arg* a = (ia_arg*)p;
+    if (!a->ps->active[i]) return;
+    long w = 0, bd = -1;
+    int rc = interact_one(a->op, a->kfamily, a->kdim, a->ps, a->ops, a->nops, a->out,
+                          a->out_comps, i, b, &w, &bd);
+    a->warns[i] = w;
+    if (rc) {
+        pthread_mutex_lock(&a->mu);
+        if (i < a->first_fail) {
+            a->first_fail = i;
+            a->fail_bad = bd;
+        }
+        pthread_mutex_unlock(&a->mu);
+    }
+}
+
+int nor_interact(int op, int kfamily, int kdim, nor_ps* ps, const nor_operand* ops, int nops,
+                 double* out, int out_comps, long* bad) {
+    const int n = ps->n;
+    ia_arg a;
+    a.op = op;
+    a.kfamily = kfamily;
+    a.kdim = kdim;
+    a.nops = nops;
+    a.out_comps = out_comps;
+    a.ps = ps;
+    a.ops = ops;
+    a.out = out;
+    a.warns = (long*)calloc((size_t)(n > 0 ? n : 1), sizeof(long));
+    pthread_mutex_init(&a.mu, NULL);
+    a.first_fail = LONG_MAX;
+    a.fail_bad = -1;
+    parallel_for(n, op == NOR_GRAVITY ? 8 : 64, ia_body, &a);
+    pthread_mutex_destroy(&a.mu);
+    long wsum = 0;
+    for (long i = 0; i < n && i <= a.first_fail; ++i) wsum += a.warns[i];
+    free(a.warns);
+    ps->warnings += wsum;
+    *bad = -1;
+    if (a.first_fail != LONG_MAX) {
+        *bad = a.fail_bad;
+        return 1;
+    }
+    return 0;
 }
 
 /* src/sfl/ast.cpp:180-191: x + xdot * dt, active particles only (case.cpp:36-40). */

@@ -151,15 +151,17 @@ class SlabRank:
         if not self.periodic:
             c0, c1 = max(c0, 0), min(c1, self.ncx)
             return self.b.select(c0, c1, ghost) if c1 > c0 else None
-        parts = []
-        if c0 < 0:
-            parts.append(self.b.select(c0 + self.ncx, self.ncx, ghost))
-            c0 = 0
-        if c1 > self.ncx:
-            parts.append(self.b.select(0, c1 - self.ncx, ghost))
-            c1 = self.ncx
-        if c1 > c0:
-            parts.append(self.b.select(c0, c1, ghost))
+        n = self.ncx
+        if c1 <= c0:
+            return None
+        if c1 - c0 >= n:
+            return self.b.select(0, n, ghost)
+        # shift the range so that 0 <= c0 < n, then split it at the seam
+        k = c0 // n
+        c0, c1 = c0 - k * n, c1 - k * n
+        parts = [self.b.select(c0, min(c1, n), ghost)]
+        if c1 > n:
+            parts.append(self.b.select(0, c1 - n, ghost))
         return self.b.cat(parts)
 
     def exchange(self):
@@ -200,9 +202,11 @@ class SlabRank:
         set holds owned particles only (ghosts are refreshed by the caller); every particle
         keeps its global id, so sums stay in the single-GPU order."""
         import torch
-        new = bounds_from_hist(self.plane_hist(owned), self.ncx, self.x.world)
+        hist = self.plane_hist(owned)
+        new = bounds_from_hist(hist, self.ncx, self.x.world)
         if new == self.bounds:
             return owned
+        total = int(hist.sum())
         self.bounds = new
         self.lo_c, self.hi_c = new[self.r], new[self.r + 1]
         self.rebalances += 1
@@ -220,6 +224,11 @@ class SlabRank:
             pending = self.x.allreduce_sum(torch.tensor([cnt], dtype=torch.int64,
                                                         device=self.x.device))
             if int(pending.item()) == 0:
+                got = self.x.allreduce_sum(torch.tensor([int(owned.shape[0])], dtype=torch.int64,
+                                                        device=self.x.device))
+                if int(got.item()) != total:  # a particle duplicated or dropped in transit
+                    raise RuntimeError(f"slab rebalance: {int(got.item())} owned rows after the "
+                                       f"hops, {total} before")
                 return owned
             keep = self.b.select(lo, hi, 0)
             from_left, from_right = self.x.swap(to_left, to_right, self.b.width)

@@ -34,17 +34,20 @@ def make_scene(kind):
         return sc, False
     # periodic x: a fluid layer over a 3-layer floor, sheared fast x-velocity so
     # particles wrap around the ring and cross both slab faces
+    # "ring30": the same layer on a 30-plane ring (re-balanced planes cross the seam)
+    planes = 30 if kind == "ring30" else 10
     base = scenes.dam_break(2, dx=0.05, fluid=(2.0, 0.5), tank=(2.0, 1.0))
     dx = 0.05
-    fx, fy = np.meshgrid((np.arange(40) + 0.5) * dx, (np.arange(10) + 0.5) * dx, indexing="xy")
-    wx, wy = np.meshgrid((np.arange(40) + 0.5) * dx, -(np.arange(3) + 0.5) * dx, indexing="xy")
+    nx = 4 * planes
+    fx, fy = np.meshgrid((np.arange(nx) + 0.5) * dx, (np.arange(10) + 0.5) * dx, indexing="xy")
+    wx, wy = np.meshgrid((np.arange(nx) + 0.5) * dx, -(np.arange(3) + 0.5) * dx, indexing="xy")
     pos = np.stack([np.concatenate([fx.ravel(), wx.ravel()]), np.concatenate([fy.ravel(), wy.ravel()])])
     n, nf = pos.shape[1], fx.size
     mask = np.zeros(n)
     mask[:nf] = 1.0
     v = np.zeros((2, n))
     v[0, :nf] = 2.0 + pos[1, :nf]
-    sc = scenes.Scene("periodic_layer", 2, [0, -1], [10, 6], [0.2, 0.2], [0, 2], pos,
+    sc = scenes.Scene("periodic_layer", 2, [0, -1], [planes, 6], [0.2, 0.2], [0, 2], pos,
                       fields={"rho": np.full(n, 1000.0), "p": np.zeros(n), "v": v,
                               "vdot": np.zeros((2, n)), "mask": mask},
                       params=dict(base.params, dt=5e-4))
@@ -119,7 +122,7 @@ def test_two_slabs_match_one_rank_bitwise(kind):
     np.testing.assert_array_equal(two, one)
 
 
-@pytest.mark.parametrize("kind,world", [("dam", 3), ("periodic", 3)])
+@pytest.mark.parametrize("kind,world", [("dam", 3), ("periodic", 3), ("ring30", 3)])
 def test_rebalanced_slabs_match_one_rank_bitwise(kind, world):
     """SURVEY.md §8(e) re-balancing: start from skewed bounds (two-plane slabs and one
     huge one), re-balance every 4 steps on the global plane histogram; bounds move by
