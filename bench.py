@@ -210,6 +210,16 @@ def stencil_candidates(ctx, dim):
     return float((g * acc).sum())
 
 
+WORKLOAD_NAMES = {
+    0: "cfg0: 2D WCSPH dam break, 20,000 fluid + 3-layer walls, dx=0.01",
+    1: "cfg1: 3D SPH operator microbench, N=1,048,576 periodic, cubic spline",
+    2: "cfg2: 3D WCSPH dam break, 4.0M fluid + 3-layer walls, dx=0.005, Wendland C2",
+    3: ("cfg3: 3D DEM granular settling, 2,000,000 spheres, log-normal radii, "
+        "linear spring-dashpot + Coulomb, dt=1e-6"),
+    4: "cfg4: 3D n-body Plummer sphere, N=262,144, eps=0.01, leapfrog dt=1e-3",
+}
+
+
 class Workload:
     name = ""
     dtype = "f64"
@@ -231,7 +241,7 @@ class Microbench(Workload):
     def __init__(self):
         from paper_1710_08259_b200 import scenes
         self.sc = scenes.sph_microbench()
-        self.name = "cfg1: 3D SPH operator microbench, N=1,048,576 periodic, cubic spline"
+        self.name = WORKLOAD_NAMES[1]
         self.kw = "Wc33220"
 
     def setup(self, ctx):
@@ -247,20 +257,26 @@ class Microbench(Workload):
         C = stencil_candidates(ctx, 3)
         nn = float(ctx.neighbor_counts(prm["radius"]).sum())
         N = float(sc.n)
-        # per-particle bytes / flops
+        nc = float(np.prod([b - a for a, b in zip(sc.min_cells, sc.max_cells)]))
+        # SURVEY.md §8(d) algorithmic bytes B and flops F per launch (per-particle figure x
+        # N): every operator pass is charged 8 flops per stencil candidate (C) plus its
+        # per-neighbour flops (n), whether or not the implementation skips candidates.
+        # The neighbour-list build is an implementation kernel: its positions read is
+        # counted, its candidate tests are already charged to the passes.
         self.kernels = {
-            100: ("sph_S density", 32.0 * N + 4.0 * nn, 14 * nn),
-            102: ("sph_G11 gradient", 64.0 * N + 4.0 * nn, 24 * nn),
-            103: ("sph_L0 Laplacian", 48.0 * N + 4.0 * nn, 27 * nn),
-            # fused G11 + L0 (one list walk): x, A, rho in; G, L out; A, m, rho at j
-            110: ("sph_G11+L0 fused", 80.0 * N + 4.0 * nn, (24 + 27) * nn),
-            302: ("neighbour-list build", 20.0 * N + 4.0 * nn, 0.0),
-            300: ("cell build", (32.0 + 60.0 + 4.0 + 16.0 * 8) * N, 0.0),
+            100: ("sph_S density", 32.0 * N, 8.0 * C + 14 * nn),
+            102: ("sph_G11 gradient", 64.0 * N, 8.0 * C + 24 * nn),
+            103: ("sph_L0 Laplacian", 48.0 * N, 8.0 * C + 27 * nn),
+            # fused G11 + L0 (one list walk): x, A, rho in; G, L out; both passes' flops
+            110: ("sph_G11+L0 fused", 80.0 * N, 2 * 8.0 * C + (24 + 27) * nn),
+            302: ("neighbour-list build", 24.0 * N, 0.0),
+            # hash 32 + sort 60 + range 4 + 8 N_c/N + reorder of r, A (16 B per component)
+            300: ("cell build", (32.0 + 60.0 + 4.0 + 16.0 * 4) * N + 8.0 * nc, 0.0),
         }
         self.cand_per_particle = C / N
         self.nbr_per_particle = nn / N
         # SURVEY.md §8(d) step roofline: 8 flops per stencil candidate per operator pass
-        self.survey = (sum(b for k, (_, b, _) in self.kernels.items() if k != 110),
+        self.survey = (sum(b for k, (_, b, _) in self.kernels.items() if k not in (110,)),
                        3 * 8.0 * C + (14 + 24 + 27) * nn,
                        "3 passes x 8C + (14 + 24 + 27) n")
         import torch
@@ -300,11 +316,10 @@ class DamBreak(Workload):
         self.dim = dim
         if dim == 3:
             self.sc = scenes.dam_break(3, dx=0.005)
-            self.name = ("cfg2: 3D WCSPH dam break, 4.0M fluid + 3-layer walls, dx=0.005, "
-                         "Wendland C2")
+            self.name = WORKLOAD_NAMES[2]
         else:
             self.sc = scenes.dam_break(2, dx=0.01)
-            self.name = "cfg0: 2D WCSPH dam break, 20,000 fluid + 3-layer walls, dx=0.01"
+            self.name = WORKLOAD_NAMES[0]
 
     def setup(self, ctx):
         from paper_1710_08259_b200 import nau
@@ -331,13 +346,19 @@ class DamBreak(Workload):
         N = float(sc.n)
         d = sc.dim
         self.n_active = sc.n
+        nc = float(np.prod([b - a for a, b in zip(sc.min_cells, sc.max_cells)]))
+        # SURVEY.md §8(d) algorithmic bytes B and flops F per launch (per-particle figure x
+        # N; 3D figures, scaled by dim): density 40 B, 8C + 14n + 10; G11 + A 88 B,
+        # 8C + 42n; integrator 128 B, 20; cell build = hash 32 + sort 60 + range 4 +
+        # 8 N_c/N + reorder 16 B per moved component (r, v, rho, mask). The neighbour-
+        # list build is an implementation kernel (positions read; its candidate tests are
+        # already charged to the two passes).
         self.kernels = {
-            # + 4 B per list entry (>= one per neighbour): the list is the passes' input
-            200: ("density+EOS", (8.0 * d + 8 + 8) * N + 4.0 * nn, 14 * nn + 10 * N),
-            201: ("momentum G11+A", (8.0 * d * 3 + 16) * N + 4.0 * nn, 42 * nn),
-            302: ("neighbour-list build", 20.0 * N + 4.0 * nn, 0.0),
+            200: ("density+EOS", (8.0 * d + 8 + 8) * N, 8.0 * C + 14 * nn + 10 * N),
+            201: ("momentum G11+A", (8.0 * d * 3 + 16) * N, 8.0 * C + 42 * nn),
+            302: ("neighbour-list build", 8.0 * d * N, 0.0),
             301: ("symplectic integrator", (8.0 * (4 * d + 1) + 8 * 2 * d) * N, 20.0 * N),
-            300: ("cell build", (8.0 * d + 8 + 60 + 4 + 16 * (3 * d + 3)) * N, 0.0),
+            300: ("cell build", (8.0 * d + 8 + 60 + 4 + 16 * (2 * d + 2)) * N + 8.0 * nc, 0.0),
         }
         self.cand_per_particle = C / N
         self.nbr_per_particle = nn / N
@@ -377,8 +398,7 @@ class DemColumn(Workload):
     def __init__(self):
         from paper_1710_08259_b200 import scenes
         self.sc = scenes.dem_column()
-        self.name = ("cfg3: 3D DEM granular settling, 2,000,000 spheres, log-normal radii, "
-                     "linear spring-dashpot + Coulomb, dt=1e-6")
+        self.name = WORKLOAD_NAMES[3]
 
     def setup(self, ctx):
         from paper_1710_08259_b200 import nau
@@ -401,12 +421,19 @@ class DemColumn(Workload):
         C = stencil_candidates(ctx, 3)
         N = float(sc.n)
         self.n_active = sc.n
+        nc = float(np.prod(sc.max_cells))
+        self._C = C
+        # DEM 88 B, 8C + 40 per contact (contacts counted below);
+        # integrator (no mask) 120 B, 20; cell build hash + sort + range + reorder of
+        # r, v, R, m (8 components)
         self.kernels = {
-            108: ("dem_lsd contact sum", 88.0 * N, 0.0),
-            301: ("symplectic integrator", 8.0 * 22 * N, 20.0 * N),
-            300: ("cell build", (24.0 + 8 + 60 + 4 + 16 * 11) * N, 0.0),
+            108: ("dem_lsd contact sum", 88.0 * N, 8.0 * C),
+            301: ("symplectic integrator", (8.0 * 9 + 8 * 6) * N, 20.0 * N),
+            300: ("cell build", (24.0 + 8 + 60 + 4 + 16 * 8) * N + 8.0 * nc, 0.0),
         }
         self.cand_per_particle = C / N
+        self.survey = (sum(b for _, b, _ in self.kernels.values()), 8.0 * C + 20.0 * N,
+                       "8C + 20 per particle (contact flops not counted)")
         import torch
         self.h_r = torch.from_numpy(np.ascontiguousarray(sc.pos)).pin_memory()
         self.h_v = torch.zeros((3, sc.n), dtype=torch.float64).pin_memory()
@@ -436,7 +463,7 @@ class Gravity(Workload):
     def __init__(self):
         from paper_1710_08259_b200 import scenes
         self.sc = scenes.plummer()
-        self.name = "cfg4: 3D n-body Plummer sphere, N=262,144, eps=0.01, leapfrog dt=1e-3"
+        self.name = WORKLOAD_NAMES[4]
 
     def setup(self, ctx):
         from paper_1710_08259_b200 import nau
@@ -797,39 +824,65 @@ def run_ours(args, dist):
     dist.barrier()
     ms_e2e = dist.max(timed_pipelined(ctx, wl.e2e_step, args.steps))
     e2e = n_total * args.steps / (ms_e2e * 1e-3)
-    # ---- roofline of the dominant kernel ----
+    # ---- roofline of the dominant kernel (SURVEY.md §8(d)) ----
+    # T* = max(B / BW_HBM, F / P_FP64) with B, F the algorithmic bytes and flops of one
+    # launch; frac = T* / T (T = mean CUDA-event launch time on the context stream).
     peaks, peak_kind = measured_peaks()
+    hbm_peak = peaks["hbm_gbs"]
     fp64_peak = nau.fp64_peak_tflops(dist.local)
+    fp64_src = ("builder-measured: nau_fp64_peak_tflops (csrc/fp64peak.cu, independent DFMA "
+                "chains on every SM) in this run; MEASURED_PEAKS.json has no FP64 figure")
     traffic = ncu_traffic(args.config if args.mode == "fast" else f"{args.config}_exact")
+
+    def tstar(B, F):
+        t_hbm = B / (hbm_peak * 1e9)
+        t_fp = F / (fp64_peak * 1e12)
+        return max(t_hbm, t_fp), ("hbm" if t_hbm >= t_fp else "fp64")
+
     per_kernel = {}
     for cls, (label, B, F) in wl.kernels.items():
         tot, cnt = prof[cls]
         if cnt == 0:
             continue
         t = tot / cnt * 1e-3
+        ts, bnd = tstar(B, F)
+        tr = traffic.get(label)
         per_kernel[label] = {"ms_per_launch": round(tot / cnt, 4), "launches": cnt,
-                             "share_of_step": round(tot / ms, 4),
-                             "GB_s": round(B / t / 1e9, 1),
-                             "fp64_TFLOP_s": round(F / t / 1e12, 3) if F else 0.0}
+                             "share_of_step": round(tot / ms, 4), "bound": bnd,
+                             "t_star_ms": round(ts * 1e3, 4), "frac": round(ts / t, 4),
+                             "algorithmic_GB_s": round(B / t / 1e9, 1),
+                             "fp64_TFLOP_s": round(F / t / 1e12, 3) if F else 0.0,
+                             "dram_bytes_ncu": tr.get("dram_bytes") if isinstance(tr, dict) else tr}
     dom_cls = max((c for c in wl.kernels if prof[c][1]), key=lambda c: prof[c][0])
     label, B, F = wl.kernels[dom_cls]
     tot, cnt = prof[dom_cls]
     t = tot / cnt * 1e-3
-    achieved = B / t / 1e9
+    ts, bnd = tstar(B, F)
     tr = traffic.get(label)
+    dram = tr.get("dram_bytes") if isinstance(tr, dict) else tr
     roofline = {
-        "kernel": label, "bound": "hbm", "achieved": round(achieved, 1),
-        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-        "traffic": tr, "peak_source": peak_kind,
+        "kernel": label, "bound": bnd,
+        "achieved": round(F / t / 1e12, 3) if bnd == "fp64" else round(B / t / 1e9, 1),
+        "peak": round(fp64_peak, 2) if bnd == "fp64" else hbm_peak,
+        "unit": "TFLOP/s" if bnd == "fp64" else "GB/s",
+        "frac": round(ts / t, 4),
+        "traffic": dram,
+        "algorithmic_bytes": B, "algorithmic_flops": F,
+        "traffic_overhead": (round(dram / B, 2) if dram else None),
+        "hbm": {"achieved_GB_s": round(B / t / 1e9, 1), "peak": hbm_peak,
+                "frac": round(B / t / 1e9 / hbm_peak, 4), "peak_source": peak_kind},
         "fp64": {"achieved_tflops": round(F / t / 1e12, 3), "peak_tflops": round(fp64_peak, 2),
-                 "frac": round(F / t / 1e12 / fp64_peak, 4),
-                 "peak_source": "measured in this run (nau_fp64_peak_tflops, DFMA chains)"},
-        "note": ("neighbour sums are FP64/latency-bound (SURVEY.md §8(d)); 'achieved' = "
-                 "algorithmic bytes / mean CUDA-event launch time"),
+                 "frac": round(F / t / 1e12 / fp64_peak, 4), "peak_source": fp64_src,
+                 "issued_flops_ncu": tr.get("fp64_flops") if isinstance(tr, dict) else None},
+        "note": ("B and F are SURVEY.md §8(d)'s per-particle figures x N (F charges 8 flops per "
+                 "stencil candidate plus the per-neighbour flops); achieved = F / mean "
+                 "CUDA-event launch time; frac = T*/T with T* = max(B/BW_HBM, F/P_FP64); "
+                 "traffic = ncu DRAM bytes per launch (profiles/traffic.json), "
+                 "traffic_overhead = traffic / B (neighbour-list and stencil re-reads)"),
     }
     if wl.survey:  # the whole step against T* = max(B / BW_HBM, F / P_FP64), SURVEY.md §8(d)
         Bs, Fs, basis = wl.survey
-        t_hbm = Bs / (peaks["hbm_gbs"] * 1e9) * 1e3
+        t_hbm = Bs / (hbm_peak * 1e9) * 1e3
         t_fp = Fs / (fp64_peak * 1e12) * 1e3
         roofline["step"] = {"t_star_ms": round(max(t_hbm, t_fp), 4), "hbm_ms": round(t_hbm, 4),
                             "fp64_ms": round(t_fp, 4),
@@ -862,7 +915,8 @@ def run_ours(args, dist):
         "clocks": clk,
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, wl)
+        line["cpu_baseline"] = cpu_baseline(args, wl, full_steps=REF_FULL_STEPS[args.config]
+                                            if args.config in (0, 2) else None)
     # torch tensors allocated inside the ExternalStream(ctx stream) regions must be
     # released before the context destroys that stream
     import gc
@@ -875,54 +929,42 @@ def run_ours(args, dist):
 
 
 # ----------------------------------------------------- CPU reference ----
-def cpu_baseline(args, wl=None):
-    """Time the reference's own CPU path (oracle/_ref) on a bounded sample."""
+def _ref_deck(config, sc):
+    """The workload as a reference Case (oracle/_ref: the unmodified reference sources),
+    assembled the way tests/helpers.hpp:26-80 does, with its equations in deck order.
+    Returns (case, equations as (name, text), components per RHS, note)."""
     from oracle import ref
-    threads = os.cpu_count() or 1
-    if not ref.available():
-        return cpu_baseline_port(args)
-    if args.config == 1:
-        from paper_1710_08259_b200 import scenes
-        sc = wl.sc if wl else scenes.sph_microbench()
-        prm = sc.params
-        rc = ref.RefCase(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds, sc.pos)
+    prm = sc.params
+    rc = ref.RefCase(sc.dim, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds, sc.pos)
+    if config == 1:
         rc.field("A", sc.fields["A"]).field("rho", np.full(sc.n, prm["rho0"]))
+        rc.field("G", np.zeros((3, sc.n))).field("L", np.zeros(sc.n))
         rc.constant("one", 1.0).constant("m", prm["mass"]).constant("R", prm["radius"])
-        exprs = ["sph_S(one,m,one,Wp53220,R)", "sph_G11(A,m,rho,Wp53220,R)",
-                 "sph_L0(A,m,rho,Wp53220,R)"]
+        eqs = [("density", "rho=sph_S(one,m,one,Wp53220,R)"),
+               ("gradient", "G=sph_G11(A,m,rho,Wp53220,R)"),
+               ("laplacian", "L=sph_L0(A,m,rho,Wp53220,R)")]
         comps = [1, 3, 1]
-        kernel_note = "Wendland Wp53220 (the reference has no cubic spline; same candidate loop)"
-    elif args.config == 3:
-        from paper_1710_08259_b200 import scenes
-        sc = wl.sc if wl else scenes.dem_column()
-        prm = sc.params
-        rc = ref.RefCase(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds, sc.pos)
+        note = "Wendland Wp53220 (the reference has no cubic spline; same candidate loop)"
+    elif config == 3:
         rng = np.random.default_rng(0)
         rc.field("v", rng.uniform(-0.01, 0.01, (3, sc.n))).field("vdot", sc.fields["vdot"])
         rc.field("R", sc.fields["R"]).field("m", sc.fields["m"])
         rc.constant("E", 2.06e6).constant("nu", 0.33).constant("cf", prm["cf"])
         rc.constant("Rs", prm["search_radius"]).constant("g", prm["g"]).variable("dt", prm["dt"])
-        exprs = ["dem_l(v,R,E,nu,m,cf,Rs)+g", "euler(v,vdot,dt)", "euler(r,v,dt)"]
+        eqs = [("accel", "vdot=dem_l(v,R,E,nu,m,cf,Rs)+g"), ("velocity", "v=euler(v,vdot,dt)"),
+               ("position", "r=euler(r,v,dt)")]
         comps = [3, 3, 3]
-        kernel_note = ("the reference's stock Hertz dem_l through the same contact loop "
-                       "(it has no linear spring-dashpot law)")
-    elif args.config == 4:
-        from paper_1710_08259_b200 import scenes
-        sc = wl.sc if wl else scenes.plummer()
-        prm = sc.params
-        rc = ref.RefCase(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds, sc.pos)
+        note = ("the reference's stock Hertz dem_l through the same contact loop "
+                "(it has no linear spring-dashpot law)")
+    elif config == 4:
         rc.field("v", sc.fields["v"]).field("a", sc.fields["a"])
         rc.constant("m", prm["m"]).constant("G", prm["G"]).constant("eps", prm["eps"])
         rc.variable("dth", 0.5 * prm["dt"]).variable("dt", prm["dt"])
-        exprs = ["euler(v,a,dth)", "euler(r,v,dt)", "nbody_gravity(m,G,eps)", "euler(v,a,dth)"]
+        eqs = [("kick1", "v=euler(v,a,dth)"), ("drift", "r=euler(r,v,dt)"),
+               ("force", "a=nbody_gravity(m,G,eps)"), ("kick2", "v=euler(v,a,dth)")]
         comps = [3, 3, 3, 3]
-        kernel_note = "nbody_gravity all pairs (interactions.cpp:195-214), leapfrog as equation order"
+        note = "nbody_gravity all pairs (interactions.cpp:195-214), leapfrog as equation order"
     else:
-        from paper_1710_08259_b200 import scenes
-        sc = wl.sc if wl else (scenes.dam_break(3, dx=0.005) if args.config == 2
-                               else scenes.dam_break(2))
-        prm = sc.params
-        rc = ref.RefCase(sc.dim, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds, sc.pos)
         rng = np.random.default_rng(0)
         vel = rng.uniform(-0.1, 0.1, (sc.dim, sc.n))  # non-zero so sph_A does its full work
         for k in ("rho", "p", "vdot", "mask"):
@@ -931,10 +973,37 @@ def cpu_baseline(args, wl=None):
         rc.constant("one", 1.0).constant("mass", prm["mass"]).constant("R", prm["radius"])
         rc.constant("B", prm["B"]).constant("rho0", prm["rho0"]).constant("gam", prm["gamma"])
         rc.constant("visc", prm["visc"]).constant("g", prm["g"]).variable("dt", prm["dt"])
-        eqs = scenes.wcsph_equations(sc)
-        exprs = [t.split("=", 1)[1] for _, t in eqs]
+        eqs = scenes_wcsph(sc)
         comps = [1, 1, sc.dim, sc.dim, sc.dim]
-        kernel_note = f"Wendland Wp5{sc.dim}220"
+        note = f"Wendland Wp5{sc.dim}220"
+    for name, text in eqs:
+        rc.equation(name, text)
+    return rc, eqs, comps, note
+
+
+def scenes_wcsph(sc):
+    from paper_1710_08259_b200 import scenes
+    return scenes.wcsph_equations(sc)
+
+
+def _scene(config):
+    from paper_1710_08259_b200 import scenes
+    return {1: scenes.sph_microbench, 2: lambda: scenes.dam_break(3, dx=0.005),
+            0: lambda: scenes.dam_break(2), 3: scenes.dem_column, 4: scenes.plummer}[config]()
+
+
+def cpu_baseline(args, wl=None, full_steps=None):
+    """Time the reference's own CPU path (oracle/_ref) on the box's host cores:
+    (1) `full_steps` full-N Case::solve_step(ThreadPool(P)) calls (SURVEY.md §8(d)'s
+    anchor; skipped when None), and (2) the bounded sample estimate: build_cells over
+    all particles + every equation's RHS over a spread sample of particles."""
+    from oracle import ref
+    threads = os.cpu_count() or 1
+    if not ref.available():
+        return cpu_baseline_port(args)
+    sc = wl.sc if wl else _scene(args.config)
+    rc, eqs, comps, kernel_note = _ref_deck(args.config, sc)
+    exprs = [t.split("=", 1)[1] for _, t in eqs]
     n = sc.n
     t0 = time.perf_counter()
     rc.build_cells()
@@ -958,18 +1027,40 @@ def cpu_baseline(args, wl=None):
     cnt2 = int(min(n, max(cnt, cnt * scale)))
     t, cnt = sample_cost(cnt2)
     per_particle = t_build / n + t / cnt
-    value = 1.0 / per_particle
+    est = 1.0 / per_particle
     try:
         model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo")
                  if l.startswith("model name")][0]
     except (OSError, IndexError):
         model = "unknown"
-    return {"value": round(value, 1), "unit": "particle-updates/s", "cores": threads,
-            "kind": "reference",
-            "sample": (f"reference Case path (oracle/_ref, unmodified sources): build_cells over all "
-                       f"{n} particles ({t_build:.2f} s, single-threaded as in the reference) + "
-                       f"every equation's RHS evaluated over {cnt} particles in 8 spread chunks on "
-                       f"ThreadPool({threads}) ({t:.2f} s); {kernel_note}; host CPU: {model}")}
+    sample = (f"sample estimate: build_cells over all {n} particles ({t_build:.2f} s, "
+              f"single-threaded as in the reference) + every equation's RHS over {cnt} particles "
+              f"in 8 spread chunks on ThreadPool({threads}) ({t:.2f} s)")
+    out = {"unit": "particle-updates/s", "cores": threads, "kind": "reference",
+           "sample_estimate": round(est, 1)}
+    if full_steps:
+        # the full deck: lazy build_cells, every equation over all N, staging, NaN audit,
+        # swap, boundary shift (Case::solve_step, case.cpp:9-67) on ThreadPool(P)
+        rc.boundary_shift()
+        ts = []
+        for _ in range(full_steps):
+            s0 = time.perf_counter()
+            rc.solve_step(threads)
+            ts.append(time.perf_counter() - s0)
+        t_full = sum(ts)
+        out["value"] = round(n * full_steps / t_full, 1)
+        out["full_steps"] = {"steps": full_steps, "seconds": round(t_full, 2),
+                             "per_step_s": [round(x, 3) for x in ts]}
+        out["sample"] = (f"reference Case path (oracle/_ref, unmodified sources): {full_steps} "
+                         f"full-N Case::solve_step(ThreadPool({threads})) over all {n} particles "
+                         f"({t_full:.2f} s; value = N x steps / that time); {sample} gives "
+                         f"{est:.4g}; {kernel_note}; host CPU: {model}")
+    else:
+        out["value"] = round(est, 1)
+        out["sample"] = (f"reference Case path (oracle/_ref, unmodified sources): {sample}; "
+                         f"{kernel_note}; host CPU: {model}")
+    del rc
+    return out
 
 
 def cpu_baseline_port(args):
@@ -977,21 +1068,25 @@ def cpu_baseline_port(args):
             "sample": "oracle/_ref not present on this machine"}
 
 
+REF_FULL_STEPS = {0: 20, 1: 1, 2: 1, 3: 2, 4: 1}
+
+
 def run_reference(args, dist):
     if dist.rank != 0:
         return None
-    wl_name = {1: "cfg1", 2: "cfg2", 0: "cfg0", 3: "cfg3", 4: "cfg4"}[args.config]
-    cb = cpu_baseline(args)
+    cb = cpu_baseline(args, full_steps=REF_FULL_STEPS[args.config])
     per_step_ms = None
+    n = _scene(args.config).n if cb["value"] else None
     if cb["value"]:
-        from paper_1710_08259_b200 import scenes
-        n = {1: lambda: scenes.sph_microbench().n, 2: lambda: scenes.dam_break(3, dx=0.005).n,
-             0: lambda: scenes.dam_break(2).n, 3: lambda: 2_000_000, 4: lambda: 262_144}[args.config]()
         per_step_ms = n / cb["value"] * 1e3
     return {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "particle-updates/s",
             "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": wl_name, "threads": cb["cores"]},
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD_NAMES[args.config], "threads": cb["cores"],
+                       "timed": (f"{cb.get('full_steps', {}).get('steps')} full-N "
+                                 "Case::solve_step call(s) on all host threads (the reference's "
+                                 "whole step; --steps/--warmup do not apply)")},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "particle-updates/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}

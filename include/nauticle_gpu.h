@@ -392,6 +392,13 @@ nau_status nau_profile_enable(nau_ctx* ctx, int on);
 double nau_profile_ms(nau_ctx* ctx, int kernel_class, long* launches);
 long nau_launch_count(nau_ctx* ctx);
 
+/* Which kernels the last nau_wcsph_step ran (tests pin the benchmarked path):
+ * bit 4 FAST mode, bits 2-3 the neighbour source (0 cell sweep, 1 per-particle
+ * lists, 2 paired lists), bit 0 an image-carrying instantiation (some axis periodic
+ * or symmetric). -1 before the first step. */
+enum { NAU_PATH_IMAGES = 1, NAU_PATH_FAST = 16 };
+int nau_wcsph_path(nau_ctx* ctx);
+
 /* Microbenchmark: measured fp64 FMA throughput (TFLOP/s) of this GPU. */
 double nau_fp64_peak_tflops(int device);
 

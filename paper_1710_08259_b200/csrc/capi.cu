@@ -930,6 +930,12 @@ nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
     const bool pairs = c->mode == NAU_MODE_FAST && p->kernel_family == NAU_K_WENDLAND &&
                        p->radius <= min_cs;
     const int lists = nau::nlist_for(c, p->radius, c->mode == NAU_MODE_EXACT, pairs);
+    {
+        int img = 0;
+        for (int a = 0; a < c->dom.dim; ++a) img |= c->dom.kind[a] != NAU_CUTOFF;
+        c->last_wcsph_path = (c->mode == NAU_MODE_FAST ? NAU_PATH_FAST : 0) | (lists << 2) |
+                             (img ? NAU_PATH_IMAGES : 0);
+    }
     if (c->mode == NAU_MODE_FAST) {
         nau::launch_wcsph_fast(c, p, c->d_aux, lists);
         nau::launch_symplectic(c, c->fields[p->f_v].d, c->fields[p->f_vdot].d,
@@ -1055,5 +1061,7 @@ double nau_profile_ms(nau_ctx* c, int cls, long* launches) {
 }
 
 long nau_launch_count(nau_ctx* c) { return c->launches; }
+
+int nau_wcsph_path(nau_ctx* c) { return c ? c->last_wcsph_path : -1; }
 
 }  // extern "C"

@@ -394,6 +394,7 @@ struct nau_ctx {
     unsigned long long rng_seed = 0;
     std::vector<IoStage> io_up, io_down;  // indexed by field id
     int mode = NAU_MODE_EXACT;
+    int last_wcsph_path = -1;  // nau_wcsph_path: which kernels the last nau_wcsph_step ran
     int* d_cell_start = nullptr;  // ncells + 2
     int* d_cell_count = nullptr;  // ncells + 1
     int* d_cursor = nullptr;      // ncells + 1

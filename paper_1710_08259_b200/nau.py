@@ -37,7 +37,7 @@ EXPORTS = [
     "nau_build_cells", "nau_cells_dirty", "nau_rebuild_count", "nau_warning_count", "nau_ncells",
     "nau_cell_tables", "nau_neighbor_counts", "nau_interact", "nau_interact_g11_l0", "nau_euler", "nau_symplectic_step",
     "nau_wcsph_step", "nau_reduce", "nau_sync", "nau_last_error", "nau_profile_enable",
-    "nau_profile_ms", "nau_launch_count", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
+    "nau_profile_ms", "nau_launch_count", "nau_wcsph_path", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
     "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows", "nau_dem_step",
     "nau_leapfrog_step", "nau_pack_sources", "nau_gravity_sources", "nau_set_neighbor_lists",
     "nau_upload_async", "nau_download_async", "nau_io_fence", "nau_io_join", "nau_eval",
@@ -143,6 +143,7 @@ def load():
         "nau_profile_enable": (i, [vp, i]),
         "nau_profile_ms": (d, [vp, i, C.POINTER(l)]),
         "nau_launch_count": (l, [vp]),
+        "nau_wcsph_path": (i, [vp]),
         "nau_fp64_peak_tflops": (d, [i]),
         "nau_set_mode": (i, [vp, i]),
         "nau_get_mode": (i, [vp]),
@@ -611,3 +612,12 @@ class Context:
     @property
     def launches(self):
         return self.L.nau_launch_count(self.h)
+
+    @property
+    def wcsph_path(self):
+        """Kernels of the last wcsph_step: dict(fast, source, images) (nau_wcsph_path)."""
+        v = self.L.nau_wcsph_path(self.h)
+        if v < 0:
+            return None
+        return {"fast": bool(v & 16), "source": ("sweep", "lists", "paired")[(v >> 2) & 3],
+                "images": bool(v & 1)}
