@@ -126,6 +126,7 @@ nau_status nau_get_active(nau_ctx* ctx, uint8_t* active);
 /* ≙ Workspace::add_field (workspace.cpp:39-48): new field of rows x cols per particle. */
 nau_status nau_alloc_field(nau_ctx* ctx, int rows, int cols, int* field_id);
 nau_status nau_free_field(nau_ctx* ctx, int field_id);
+nau_status nau_field_shape(nau_ctx* ctx, int field_id, int* rows, int* cols);
 /* host SoA, component-major [c*n + i] with c = col*rows + row, original order */
 nau_status nau_upload(nau_ctx* ctx, int field_id, const double* soa, long n);
 nau_status nau_download(nau_ctx* ctx, int field_id, double* soa, long n);
@@ -301,6 +302,40 @@ nau_status nau_set_random_state(nau_ctx* ctx, unsigned long long seed,
                                 const unsigned long long* counters);
 nau_status nau_get_random_counters(nau_ctx* ctx, unsigned long long* counters);
 
+/* ---- host equation executor (≙ Case::solve_equation / Case::solve_step,
+ * case.cpp:9-67; the §8(b) "Caller"; csrc/executor.cpp) ----
+ * Runs an arbitrary deck's equation list on the device: each equation's text
+ * ("lhs=rhs", the reference's canonical Equation::to_text form) is parsed with the
+ * reference's SFL grammar (sfl/parser.cpp) against the case's symbols; every solve
+ * folds uniform subtrees on the host (constants, variables, literals, frozen
+ * reductions), runs interactions through nau_interact into temporaries (operand
+ * subtrees materialised once per equation), reductions through nau_reduce +
+ * nau_allreduce, and the particle-wise rest as one nau_eval program into the LHS
+ * field (two-phase, NaN audit, boundary shift after r). A variable LHS takes the
+ * value at particle 0 (case.cpp:19-29). Errors: the reference's kinds and messages,
+ * prefixed "equation '<name>': "; nau_case_last_error gives the text and the
+ * first bad particle. Extensions over the reference's grammar: the cubic-spline
+ * keywords (Wc1D220..Wc3D220) and the dem_lsd law. Not supported: rand() inside an
+ * interaction operand (the reference draws it per neighbour). */
+typedef struct nau_case nau_case;
+nau_status nau_case_create(nau_ctx* ctx, nau_case** out); /* after nau_set_particles */
+void nau_case_destroy(nau_case* cs);
+/* Uniform symbols: rows x cols <= 3 x 3, column-major. */
+nau_status nau_case_constant(nau_case* cs, const char* name, int rows, int cols, const double* v);
+nau_status nau_case_variable(nau_case* cs, const char* name, int rows, int cols, const double* v);
+nau_status nau_case_set_variable(nau_case* cs, const char* name, int rows, int cols,
+                                 const double* v);
+nau_status nau_case_get_variable(nau_case* cs, const char* name, double* v /* 9 */, int* rows,
+                                 int* cols);
+/* Names a context field (nau_alloc_field id); "r" is field 0 and always defined. */
+nau_status nau_case_field(nau_case* cs, const char* name, int field_id);
+/* Appends an equation (parsed now; symbols must already be defined). */
+nau_status nau_case_equation(nau_case* cs, const char* name, const char* text);
+int nau_case_equation_count(nau_case* cs);
+nau_status nau_case_solve_equation(nau_case* cs, int index);
+nau_status nau_case_solve_step(nau_case* cs); /* every equation in order */
+const char* nau_case_last_error(nau_case* cs, long* first_bad_particle);
+
 /* ---- multi-GPU slab decomposition (no reference counterpart:
  * the reference has no domain decomposition) ----
  * Rows are particle-major: every live field in id order (r first), rows x cols
@@ -337,6 +372,12 @@ nau_status nau_migrate(nau_ctx* ctx);
 /* The first / last ghost_planes owned planes go to the neighbours; the context
  * then holds owned + ghost particles (ghost flag 1). Syncs. */
 nau_status nau_halo_exchange(nau_ctx* ctx);
+/* ≙ the ncclAllReduce of SURVEY.md §8(e) "Reductions": host values combined over the
+ * ranks of the context's communicator (op 0 sum, 1 max, 2 min), in place. Without a
+ * communicator (or on one rank) the values are left as they are. Syncs. */
+nau_status nau_allreduce(nau_ctx* ctx, double* values, int count, int op);
+/* Ranks of the context's communicator (1 without nau_comm_init). */
+int nau_comm_size(nau_ctx* ctx);
 /* The primitive under both: swap device row blocks (width doubles per row) with
  * the left / right neighbours; received blocks stay valid until the next call. */
 nau_status nau_comm_swap(nau_ctx* ctx, const double* to_left, long n_left, const double* to_right,

@@ -52,6 +52,13 @@ def lib():
         L.nref_neighbor_counts.argtypes = [vp, d, vp]
         L.nref_kernel_value.restype = d
         L.nref_kernel_value.argtypes = [cp, d, d]
+        L.nref_assemble.restype = vp
+        L.nref_assemble.argtypes = [C.POINTER(cp), C.POINTER(cp), C.POINTER(cp), i, C.c_uint64]
+        L.nref_domain.argtypes = [vp, C.POINTER(i), vp, vp, vp, vp]
+        L.nref_symbol.argtypes = [vp, i, i, cp, i, C.POINTER(i), C.POINTER(i), vp]
+        L.nref_equation.argtypes = [vp, i, cp, i, cp, i]
+        L.nref_rand_counters.argtypes = [vp, C.POINTER(C.c_uint64), vp]
+        L.nref_get_variable.argtypes = [vp, cp, vp, C.POINTER(i), C.POINTER(i)]
         _lib = L
     return _lib
 
@@ -194,3 +201,92 @@ class RefCase:
         out = np.empty(self.n, np.int32)
         _check(lib().nref_neighbor_counts(self.h, radius, _p(out)))
         return out
+
+
+def _cstrs(items):
+    arr = (C.c_char_p * max(1, len(items)))(*[x.encode() for x in items])
+    return arr
+
+
+class AssembledCase(RefCase):
+    """A whole deck through the reference's own assemble_case (src/assemble.cpp): the
+    document bindings come from the deck file (parsed by the caller; the reference's
+    yaml-cpp reader is the one source left out of oracle/_ref)."""
+
+    def __init__(self, items, seed=0):
+        secs, names, exprs = zip(*items) if items else ((), (), ())
+        keep = [_cstrs(list(secs)), _cstrs(list(names)), _cstrs(list(exprs))]
+        h = lib().nref_assemble(keep[0], keep[1], keep[2], len(items), C.c_uint64(seed))
+        if not h:
+            raise RefError(lib().nref_last_error().decode())
+        self.h = h
+        dim = C.c_int(0)
+        mn, mx = np.zeros(3, np.int32), np.zeros(3, np.int32)
+        cs, kd = np.zeros(3), np.zeros(3, np.int32)
+        self.n = lib().nref_domain(h, C.byref(dim), _p(mn), _p(mx), _p(cs), _p(kd))
+        self.dim = dim.value
+        d = self.dim
+        self.domain = {"dim": d, "min_cells": mn[:d].tolist(), "max_cells": mx[:d].tolist(),
+                       "cell_size": cs[:d].tolist(), "kinds": kd[:d].tolist()}
+
+    def symbols(self, kind):
+        """kind 0 constants, 1 variables, 2 fields: [(name, value (rows, cols) or shape)]."""
+        out = []
+        name = C.create_string_buffer(256)
+        r, c = C.c_int(0), C.c_int(0)
+        cnt = lib().nref_symbol(self.h, kind, -1, name, 256, C.byref(r), C.byref(c), None)
+        for k in range(cnt):
+            v = np.zeros(9)
+            lib().nref_symbol(self.h, kind, k, name, 256, C.byref(r), C.byref(c), _p(v))
+            val = v[: r.value * c.value].reshape(c.value, r.value).T.copy()
+            out.append((name.value.decode(), val if kind < 2 else (r.value, c.value)))
+        return out
+
+    def equations(self):
+        nb, tb = C.create_string_buffer(256), C.create_string_buffer(4096)
+        cnt = lib().nref_equation(self.h, -1, nb, 256, tb, 4096)
+        out = []
+        for k in range(cnt):
+            lib().nref_equation(self.h, k, nb, 256, tb, 4096)
+            out.append((nb.value.decode(), tb.value.decode()))
+        return out
+
+    def rand_state(self):
+        seed = C.c_uint64(0)
+        cnt = np.zeros(self.n, np.uint64)
+        lib().nref_rand_counters(self.h, C.byref(seed), _p(cnt))
+        return seed.value, cnt
+
+    def get_variable(self, name):
+        v = np.zeros(9)
+        r, c = C.c_int(0), C.c_int(0)
+        k = lib().nref_get_variable(self.h, name.encode(), _p(v), C.byref(r), C.byref(c))
+        if k < 0:
+            raise RefError(lib().nref_last_error().decode())
+        return v[:k].reshape(c.value, r.value).T.copy()
+
+
+def deck_items(path):
+    """CaseDocument bindings of a deck file, in document order (the schema of
+    io/case_file.cpp; scalars kept as the file's text)."""
+    import yaml
+    with open(path) as f:
+        doc = yaml.load(f, Loader=yaml.BaseLoader)
+    case = doc["simulation"]["case"]
+    ws = case["workspace"]
+    items = []
+    for sec, key in (("constant", "constants"), ("variable", "variables"), ("field", "fields")):
+        for b in ws.get(key, []) or []:
+            (name, expr), = b.items()
+            items.append((sec, name, expr))
+    ps = ws["particle_system"]
+    for k, v in ps["domain"].items():
+        items.append(("domain", k, v))
+    for k, v in ps["grid"].items():
+        items.append(("grid", k, v))
+    for b in case.get("equations", []) or []:
+        (name, expr), = b.items()
+        items.append(("equation", name, expr))
+    for k, v in (doc["simulation"].get("parameter_space") or {}).items():
+        items.append(("param", k, v))
+    return items

@@ -21,6 +21,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <functional>
@@ -41,7 +42,9 @@
 #include "nauticle/particle_system.hpp"
 #undef private
 
+#include "nauticle/assemble.hpp"
 #include "nauticle/case.hpp"
+#include "nauticle/io/case_document.hpp"
 #include "nauticle/error.hpp"
 #include "nauticle/interactions.hpp"
 #include "nauticle/io/vtk.hpp"
@@ -504,6 +507,135 @@ int nref_neighbor_counts(void* p, double radius, int* counts) {
         }
         return 0;
     } catch (const std::exception& e) { return fail(e); }
+}
+
+
+// ---- whole decks: assemble_case (src/assemble.cpp) from a CaseDocument whose
+// bindings the caller parsed from a deck file (the reference's YAML reader is the
+// one source file left out: yaml-cpp is absent). sections[k] is one of
+// "constant", "variable", "field", "equation" (name = binding name, expr = text),
+// "domain" (name in cell_size / minimum / maximum / boundary), "grid" (gid / gpos /
+// gsize / goffset / gip_dist), "param" (simulated_time / print_interval).
+void* nref_assemble(const char* const* sections, const char* const* names,
+                    const char* const* exprs, int count, uint64_t seed) {
+    try {
+        CaseDocument doc;
+        for (int k = 0; k < count; ++k) {
+            const std::string sec = sections[k], name = names[k], expr = exprs[k];
+            if (sec == "constant") doc.constants.push_back({name, expr});
+            else if (sec == "variable") doc.variables.push_back({name, expr});
+            else if (sec == "field") doc.fields.push_back({name, expr});
+            else if (sec == "equation") doc.equations.push_back({name, expr});
+            else if (sec == "domain") {
+                if (name == "cell_size") doc.cell_size = expr;
+                else if (name == "minimum") doc.minimum = expr;
+                else if (name == "maximum") doc.maximum = expr;
+                else if (name == "boundary") doc.boundary = expr;
+                else throw runtime_error("nref_assemble: domain key ", name);
+            } else if (sec == "grid") {
+                if (name == "gid") doc.grid_gid = expr;
+                else if (name == "gpos") doc.gpos = expr;
+                else if (name == "gsize") doc.gsize = expr;
+                else if (name == "goffset") doc.goffset = expr;
+                else if (name == "gip_dist") doc.gip_dist = expr;
+                else throw runtime_error("nref_assemble: grid key ", name);
+            } else if (sec == "param") {
+                if (name == "simulated_time") doc.simulated_time = expr;
+                else if (name == "print_interval") doc.print_interval = expr;
+            } else {
+                throw runtime_error("nref_assemble: section ", sec);
+            }
+        }
+        AssembleOptions opts;
+        opts.seed = seed;
+        auto h = std::make_unique<Ref>();
+        h->cs = assemble_case(doc, opts);
+        return h.release();
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
+// Domain of the assembled case: dim, min/max cells, cell sizes, kinds (3 each), N.
+int nref_domain(void* p, int* dim, int* min_cells, int* max_cells, double* cell_size,
+                int* kinds) {
+    const ParticleSystem& ps = *static_cast<Ref*>(p)->cs->workspace.particle_system();
+    const Domain& d = ps.domain();
+    *dim = d.dimension();
+    for (int a = 0; a < 3; ++a) {
+        min_cells[a] = d.min_cells_[a];
+        max_cells[a] = d.max_cells_[a];
+        cell_size[a] = d.cell_size(a);
+        kinds[a] = static_cast<int>(d.boundary(a));
+    }
+    return ps.particle_count();
+}
+
+// Symbols in definition order: kind 0 constants, 1 variables, 2 fields. Returns the
+// count; for k < count writes the name (NUL-terminated, <= cap) and rows/cols, and
+// for constants/variables the value (column-major, 9 doubles).
+int nref_symbol(void* p, int kind, int k, char* name, int cap, int* rows, int* cols,
+                double* value) {
+    Workspace& ws = static_cast<Ref*>(p)->cs->workspace;
+    auto out = [&](const std::string& nm, const Tensor& t) {
+        std::snprintf(name, cap, "%s", nm.c_str());
+        *rows = t.rows();
+        *cols = t.cols();
+        if (value)
+            for (int c = 0; c < t.cols(); ++c)
+                for (int r = 0; r < t.rows(); ++r) value[c * t.rows() + r] = t(r, c);
+    };
+    if (kind == 0) {
+        const auto& v = ws.constants();
+        if (k >= 0 && k < (int)v.size()) out(v[k]->name, v[k]->value);
+        return (int)v.size();
+    }
+    if (kind == 1) {
+        const auto& v = ws.variables();
+        if (k >= 0 && k < (int)v.size()) out(v[k]->name, v[k]->value);
+        return (int)v.size();
+    }
+    const auto& v = ws.fields();
+    if (k >= 0 && k < (int)v.size())
+        out(v[k]->name, v[k]->values.empty() ? Tensor(0.0) : v[k]->values[0]);
+    return (int)v.size();
+}
+
+// Equation k as (name, "lhs=rhs" in the reference's canonical printed form).
+int nref_equation(void* p, int k, char* name, int ncap, char* text, int tcap) {
+    const auto& eqs = static_cast<Ref*>(p)->cs->equations;
+    if (k >= 0 && k < (int)eqs.size()) {
+        std::snprintf(name, ncap, "%s", eqs[k].name.c_str());
+        std::snprintf(text, tcap, "%s=%s", eqs[k].lhs_name().c_str(), eqs[k].rhs->to_text().c_str());
+    }
+    return (int)eqs.size();
+}
+
+// The case's rand stream state (per-particle draw counters) and seed.
+int nref_rand_counters(void* p, uint64_t* seed, uint64_t* counters) {
+    Case& cs = *static_cast<Ref*>(p)->cs;
+    *seed = cs.random.seed();
+    const int n = cs.workspace.particle_count();
+    const auto& cnt = cs.random.counters();
+    for (int i = 0; i < n && counters; ++i) counters[i] = i < (int)cnt.size() ? cnt[i] : 0;
+    return n;
+}
+
+// Variable value (column-major, <= 9) after solving; returns rows*cols or -1.
+int nref_get_variable(void* p, const char* name, double* value, int* rows, int* cols) {
+    try {
+        Variable* v = static_cast<Ref*>(p)->cs->workspace.find_variable(name);
+        if (!v) throw runtime_error("nref: no variable ", name);
+        *rows = v->value.rows();
+        *cols = v->value.cols();
+        for (int c = 0; c < *cols; ++c)
+            for (int r = 0; r < *rows; ++r) value[c * *rows + r] = v->value(r, c);
+        return *rows * *cols;
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1;
+    }
 }
 
 // Wendland kernel of the reference (kernel.cpp:37-69) for KATs.

@@ -520,6 +520,13 @@ nau_status nau_alloc_field(nau_ctx* c, int rows, int cols, int* field_id) {
     return NAU_OK;
 }
 
+nau_status nau_field_shape(nau_ctx* c, int id, int* rows, int* cols) {
+    if (!field_ok(c, id)) return fail(c, NAU_ERR_ARG, "bad field id");
+    *rows = c->fields[id].rows;
+    *cols = c->fields[id].cols;
+    return NAU_OK;
+}
+
 nau_status nau_free_field(nau_ctx* c, int id) {
     if (id <= 0 || !field_ok(c, id)) return fail(c, NAU_ERR_ARG, "bad field id");
     cudaStreamSynchronize(c->stream);

@@ -44,6 +44,8 @@ struct NcclApi {
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -68,6 +70,7 @@ const NcclApi& nccl() {
         a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
         a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
         a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+        a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
         a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
         a.ok = a.why.empty();
         return a;
@@ -114,6 +117,7 @@ struct SlabComm {
     DevBuf<int> slots;
     DevBuf<double> send_l, send_r, recv_l, recv_r, all, keep;
     DevBuf<long long> counts;  // 4: send left/right, recv right/left
+    DevBuf<double> red;        // nau_allreduce staging
 };
 
 }  // namespace nau
@@ -154,16 +158,14 @@ nau_status select_range(nau_ctx* c, SlabComm& s, int c0, int c1, double ghost, l
         return st;
     };
     if (!s.periodic) return one(std::max(c0, 0), std::min(c1, s.ncx));
-    nau_status st = NAU_OK;
-    if (c0 < 0) {
-        st = one(c0 + s.ncx, s.ncx);
-        c0 = 0;
-    }
-    if (st == NAU_OK && c1 > s.ncx) {
-        st = one(0, c1 - s.ncx);
-        c1 = s.ncx;
-    }
-    if (st == NAU_OK) st = one(c0, c1);
+    if (c1 <= c0) return NAU_OK;
+    if (c1 - c0 >= s.ncx) return one(0, s.ncx);
+    // shift into the ring (0 <= c0 < ncx), then split at the seam
+    const int k = (c0 >= 0 ? c0 : c0 - s.ncx + 1) / s.ncx;
+    c0 -= k * s.ncx;
+    c1 -= k * s.ncx;
+    nau_status st = one(c0, std::min(c1, s.ncx));
+    if (st == NAU_OK && c1 > s.ncx) st = one(0, c1 - s.ncx);
     return st;
 }
 
@@ -221,6 +223,7 @@ void nau_comm_destroy(nau_ctx* c) {
     s->all.release();
     s->keep.release();
     s->counts.release();
+    s->red.release();
     delete s;
     c->slab = nullptr;
 }
@@ -321,6 +324,26 @@ static nau_status load_blocks(nau_ctx* c, SlabComm* s, const double* const* blk,
     }
     return nau_load_rows(c, s->all.p, tot, s->gid_field);
 }
+
+nau_status nau_allreduce(nau_ctx* c, double* values, int count, int op) {
+    if (!c || count < 0 || op < 0 || op > 2) return NAU_ERR_ARG;
+    SlabComm* s = c->slab;
+    if (!s || s->nranks == 1 || count == 0) return NAU_OK;  // one rank: the local value
+    if (!nau::nccl().AllReduce) return comm_fail(c, NAU_ERR_COMM, "NCCL has no ncclAllReduce");
+    if (s->red.reserve((size_t)count) != cudaSuccess)
+        return comm_fail(c, NAU_ERR_CUDA, "allreduce: out of device memory");
+    const ncclRedOp_t rop = op == 0 ? ncclSum : (op == 1 ? ncclMax : ncclMin);
+    cudaMemcpyAsync(s->red.p, values, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream);
+    nau_status st = nccl_check(c, nau::nccl().AllReduce(s->red.p, s->red.p, (size_t)count,
+                                                         ncclFloat64, rop, s->comm, c->stream),
+                               "ncclAllReduce");
+    cudaMemcpyAsync(values, s->red.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (st == NAU_OK && e != cudaSuccess) return comm_fail(c, NAU_ERR_CUDA, cudaGetErrorString(e));
+    return st;
+}
+
+int nau_comm_size(nau_ctx* c) { return c && c->slab ? c->slab->nranks : 1; }
 
 nau_status nau_migrate(nau_ctx* c) {
     SlabComm* s = c->slab;

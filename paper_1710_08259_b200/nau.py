@@ -45,6 +45,10 @@ EXPORTS = [
     "nau_comm_destroy", "nau_slab_config", "nau_migrate", "nau_halo_exchange", "nau_comm_swap",
     "nau_write_vtk", "nau_vtk_read", "nau_vtk_free", "nau_vtk_last_error", "nau_vtk_points",
     "nau_vtk_array_count", "nau_vtk_array", "nau_vtk_strings", "nau_vtk_rand_counters",
+    "nau_allreduce", "nau_comm_size", "nau_field_shape", "nau_case_create", "nau_case_destroy",
+    "nau_case_constant", "nau_case_variable", "nau_case_set_variable", "nau_case_get_variable",
+    "nau_case_field", "nau_case_equation", "nau_case_equation_count", "nau_case_solve_equation",
+    "nau_case_solve_step", "nau_case_last_error",
 ]
 
 
@@ -179,6 +183,21 @@ def load():
         "nau_vtk_array": (C.c_char_p, [vp, i, vp, vp, vp]),
         "nau_vtk_strings": (i, [vp, C.c_char_p, vp]),
         "nau_vtk_rand_counters": (l, [vp, vp]),
+        "nau_allreduce": (i, [vp, vp, i, i]),
+        "nau_comm_size": (i, [vp]),
+        "nau_field_shape": (i, [vp, i, C.POINTER(i), C.POINTER(i)]),
+        "nau_case_create": (i, [vp, C.POINTER(vp)]),
+        "nau_case_destroy": (None, [vp]),
+        "nau_case_constant": (i, [vp, C.c_char_p, i, i, vp]),
+        "nau_case_variable": (i, [vp, C.c_char_p, i, i, vp]),
+        "nau_case_set_variable": (i, [vp, C.c_char_p, i, i, vp]),
+        "nau_case_get_variable": (i, [vp, C.c_char_p, vp, C.POINTER(i), C.POINTER(i)]),
+        "nau_case_field": (i, [vp, C.c_char_p, i]),
+        "nau_case_equation": (i, [vp, C.c_char_p, C.c_char_p]),
+        "nau_case_equation_count": (i, [vp]),
+        "nau_case_solve_equation": (i, [vp, i]),
+        "nau_case_solve_step": (i, [vp]),
+        "nau_case_last_error": (C.c_char_p, [vp, C.POINTER(l)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -338,6 +357,8 @@ class Context:
         return out[0], out[1]
 
     def close(self):
+        for cs in getattr(self, "_cases", []):
+            cs.close()  # executors free their temporaries in this context first
         if getattr(self, "h", None):
             self.L.nau_destroy(self.h)
             self.h = None
@@ -621,3 +642,88 @@ class Context:
             return None
         return {"fast": bool(v & 16), "source": ("sweep", "lists", "paired")[(v >> 2) & 3],
                 "images": bool(v & 1)}
+
+
+class Case:
+    """The device equation executor (nau_case_*, csrc/executor.cpp): an arbitrary deck's
+    equation list solved with Case::solve_step semantics (case.cpp:9-67) on a Context.
+    Symbols: constants/variables are uniform tensors, fields name Context fields."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+        self.L = ctx.L
+        h = C.c_void_p()
+        st = self.L.nau_case_create(ctx.h, C.byref(h))
+        if st != 0:
+            raise NauError(st, "nau_case_create: set particles first")
+        self.h = h
+        if not hasattr(ctx, "_cases"):
+            ctx._cases = []
+        ctx._cases.append(self)
+        for name, f in ctx.fields.items():
+            if name != "r":
+                self._check(self.L.nau_case_field(self.h, name.encode(), f.id))
+
+    def _check(self, st):
+        if st != 0:
+            bad = C.c_long(-1)
+            msg = self.L.nau_case_last_error(self.h, C.byref(bad)).decode()
+            raise NauError(st, msg, bad.value)
+
+    @staticmethod
+    def _tensor(value):
+        a = np.asarray(value, dtype=np.float64)
+        if a.ndim == 0:
+            a = a.reshape(1, 1)
+        elif a.ndim == 1:
+            a = a.reshape(-1, 1)  # a python vector is a column
+        flat = np.zeros(9)
+        flat[: a.size] = a.ravel(order="F")
+        return a.shape[0], a.shape[1], flat
+
+    def constant(self, name, value):
+        r, c, v = self._tensor(value)
+        self._check(self.L.nau_case_constant(self.h, name.encode(), r, c, _p(v)))
+        return self
+
+    def variable(self, name, value):
+        r, c, v = self._tensor(value)
+        self._check(self.L.nau_case_variable(self.h, name.encode(), r, c, _p(v)))
+        return self
+
+    def set_variable(self, name, value):
+        r, c, v = self._tensor(value)
+        self._check(self.L.nau_case_set_variable(self.h, name.encode(), r, c, _p(v)))
+
+    def get_variable(self, name):
+        v = np.zeros(9)
+        r, c = C.c_int(0), C.c_int(0)
+        self._check(self.L.nau_case_get_variable(self.h, name.encode(), _p(v), C.byref(r),
+                                                 C.byref(c)))
+        return v[: r.value * c.value].reshape(c.value, r.value).T.copy()
+
+    def field(self, name, fid=None):
+        f = self.ctx.fields[name] if fid is None else fid
+        self._check(self.L.nau_case_field(self.h, name.encode(), self.ctx._fid(f)))
+        return self
+
+    def equation(self, name, text):
+        self._check(self.L.nau_case_equation(self.h, name.encode(), text.encode()))
+        return self
+
+    def solve_equation(self, k):
+        self._check(self.L.nau_case_solve_equation(self.h, k))
+
+    def solve_step(self):
+        self._check(self.L.nau_case_solve_step(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.nau_case_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
