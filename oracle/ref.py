@@ -52,6 +52,8 @@ def lib():
         L.nref_neighbor_counts.argtypes = [vp, d, vp]
         L.nref_kernel_value.restype = d
         L.nref_kernel_value.argtypes = [cp, d, d]
+        L.nref_case_ptr.restype = vp
+        L.nref_case_ptr.argtypes = [vp]
         L.nref_assemble.restype = vp
         L.nref_assemble.argtypes = [C.POINTER(cp), C.POINTER(cp), C.POINTER(cp), i, C.c_uint64]
         L.nref_domain.argtypes = [vp, C.POINTER(i), vp, vp, vp, vp]
@@ -143,6 +145,10 @@ class RefCase:
     def equation(self, name, text):
         _check(lib().nref_add_equation(self.h, name.encode(), text.encode()))
         return self
+
+    def case_ptr(self):
+        """The reference Case object (for integration/gpu_case.cpp's tests)."""
+        return lib().nref_case_ptr(self.h)
 
     def write_vtk(self, path, binary, frame_index=0, time=0.0, simulated_time=0.0):
         """The reference's make_frame + write_vtk (io/vtk.cpp:193-304)."""

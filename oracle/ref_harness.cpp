@@ -557,6 +557,9 @@ void* nref_assemble(const char* const* sections, const char* const* names,
     }
 }
 
+// The Case behind a handle (for the reference-side GPU binding's tests, integration/).
+void* nref_case_ptr(void* p) { return static_cast<Ref*>(p)->cs.get(); }
+
 // Domain of the assembled case: dim, min/max cells, cell sizes, kinds (3 each), N.
 int nref_domain(void* p, int* dim, int* min_cells, int* max_cells, double* cell_size,
                 int* kinds) {

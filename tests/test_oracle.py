@@ -201,3 +201,35 @@ def test_lsd_restitution_head_on():
         v = v + dt * a
         x = x + dt * v
     assert v[0, 1] - v[0, 0] == pytest.approx(0.5 * 1.0, rel=2e-3)
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_deck_fixtures_rebuild_through_the_public_api():
+    """tests/golden/decks.npz (the reference's shipped decks, assembled by assemble_case)
+    rebuilt through the reference's public API (Workspace fields, constants, variables,
+    parsed equations — what tests/test_gpu_binding.py hands to GpuCase) steps bitwise
+    like the assembled decks."""
+    import json
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    Z = np.load(os.path.join(os.path.dirname(__file__), "golden", "decks.npz"))
+    for deck in json.loads(str(Z["index"]))["decks"]:
+        meta = json.loads(str(Z[f"{deck}_meta"]))
+        d = meta["domain"]
+        rc = ref.RefCase(d["dim"], d["min_cells"], d["max_cells"], d["cell_size"], d["kinds"],
+                         Z[f"{deck}_s0_r"], seed=meta["seed"])
+        for name, shape in meta["fields"]:
+            if name != "r":
+                rc.field(name, Z[f"{deck}_s0_{name}"], rows=shape[0], cols=shape[1])
+        for name, v in meta["constants"]:
+            rc.constant(name, np.array(v))
+        for name, v in meta["variables"]:
+            rc.variable(name, np.array(v))
+        for name, text in meta["equations"]:
+            rc.equation(name, text)
+        for s in range(1, max(meta["steps"]) + 1):
+            rc.solve_step(1)
+            if s in meta["steps"]:
+                for name, _ in meta["fields"]:
+                    np.testing.assert_array_equal(rc.get(name), Z[f"{deck}_s{s}_{name}"],
+                                                  err_msg=f"{deck} step {s} {name}")
