@@ -374,7 +374,7 @@ nau_status nau_migrate(nau_ctx* ctx);
 nau_status nau_halo_exchange(nau_ctx* ctx);
 /* ≙ the ncclAllReduce of SURVEY.md §8(e) "Reductions": host values combined over the
  * ranks of the context's communicator (op 0 sum, 1 max, 2 min), in place. Without a
- * communicator (or on one rank) the values are left as they are. Syncs. */
+ * communicator the values are left as they are. Syncs. */
 nau_status nau_allreduce(nau_ctx* ctx, double* values, int count, int op);
 /* Ranks of the context's communicator (1 without nau_comm_init). */
 int nau_comm_size(nau_ctx* ctx);

@@ -469,6 +469,7 @@ nau_status nau_set_particles(nau_ctx* c, long n, const double* pos_soa) {
     c->rebuild_count = 0;
     c->nl_rev = -1;  // neighbour-list and fp16 caches belong to the old particle set
     c->hq_rev = -1;
+    c->xl_rev = -1;
     c->warnings = 0;
     return collect(c);
 }
@@ -890,7 +891,12 @@ nau_status nau_interact_g11_l0(nau_ctx* c, int kf, int kdim, const nau_operand* 
     bool lists = false;
     if (ops[3].field_id < 0 && ops[3].value[0] > 0.0)
         lists = nau::nlist_for(c, ops[3].value[0], false);
-    nau::launch_g11_l0_fast(c, kf, kdim, d_ops, c->fields[out_g].d, c->fields[out_l].d, lists);
+    // sph_L0 goes to the twin buffer and is committed only if nothing failed: after a
+    // sph_G11 error (or its NaN audit) the reference never evaluates the sph_L0 equation,
+    // and after an sph_L0 NaN its staging is discarded (case.cpp:46-57) — L keeps its values.
+    FieldBuf& fl = c->fields[out_l];
+    nau::launch_g11_l0_fast(c, kf, kdim, d_ops, c->fields[out_g].d, fl.alt, lists);
+    nau::launch_commit_if_ok(c, fl.alt, fl.d);
     return NAU_OK;
 }
 
@@ -927,6 +933,9 @@ nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
         if (!(k == 4 && ids[k] < 0) && !field_ok(c, ids[k])) return fail(c, NAU_ERR_ARG, "bad field id");
     if (!(p->radius > 0.0)) return fail(c, NAU_ERR_RUNTIME, "influence radius must be positive");
     if (c->dirty || !c->built_once) {
+        // rho, p (density pass) and vdot (momentum pass) are written for every active
+        // particle before anything reads them: the build moves their inactive slots only
+        c->reorder_skip = (1ULL << p->f_rho) | (1ULL << p->f_p) | (1ULL << p->f_vdot);
         nau_status s = nau_build_cells(c);
         if (s != NAU_OK) return s;
     }
@@ -969,6 +978,7 @@ nau_status nau_dem_step(nau_ctx* c, const nau_dem_params* p) {
         (p->f_m >= 0 && !field_ok(c, p->f_m)))
         return fail(c, NAU_ERR_ARG, "bad field id");
     if (c->dirty || !c->built_once) {
+        c->reorder_skip = 1ULL << p->f_vdot;  // written by the contact sum before any read
         nau_status s = nau_build_cells(c);
         if (s != NAU_OK) return s;
     }

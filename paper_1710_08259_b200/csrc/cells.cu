@@ -53,31 +53,53 @@ __global__ void k_boundary_shift(DomainDev d, long n, double* pos, uint8_t* acti
 // slots mostly share a cell, so per-particle atomics serialise on one address
 // (cfg2, 64 per cell: hash + scatter 0.27 -> 0.17 ms); at a few particles per
 // cell the match costs more than it saves (cfg3: +5%), see build_cells.
+// KH slots per thread, strided by the block size (each stride is one run of
+// consecutive slots, so the warp aggregation still sees neighbours): all loads of
+// a thread are issued before the first dependent use.
+constexpr int kHashIlp = 4;
+
 template <bool AGG>
 __global__ void k_hash(DomainDev d, long n, const double* pos, const uint8_t* active,
                        const int* orig, int* key, int* count, DevErr* err) {
-    const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    const bool valid = k < n;
-    int flat = d.ncells;
-    if (valid && active[k]) {
-        flat = 0;
-        for (int a = d.dim - 1; a >= 0; --a) {
-            double x = pos[a * n + k];
-            if (d.kind[a] == NAU_CUTOFF && (x < d.lo[a] || x > d.hi[a]))
-                latch_error(err, 4, kMsgOutsideCutoff, orig[k]);
-            flat = flat * d.cells[a] + cell_index(d, a, x);
+    const long base = (long)blockIdx.x * blockDim.x * kHashIlp + threadIdx.x;
+    double x[kHashIlp][3];
+    bool act[kHashIlp];
+#pragma unroll
+    for (int u = 0; u < kHashIlp; ++u) {
+        const long k = base + (long)u * blockDim.x;
+        const bool valid = k < n;
+        act[u] = valid && active[k];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) x[u][a] = (valid && a < d.dim) ? pos[a * n + k] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kHashIlp; ++u) {
+        const long k = base + (long)u * blockDim.x;
+        const bool valid = k < n;
+        int flat = d.ncells;
+        if (act[u]) {
+            flat = 0;
+#pragma unroll
+            for (int a = 2; a >= 0; --a) {
+                if (a >= d.dim) continue;
+                const double xa = x[u][a];
+                if (d.kind[a] == NAU_CUTOFF && (xa < d.lo[a] || xa > d.hi[a]))
+                    latch_error(err, 4, kMsgOutsideCutoff, orig[k]);
+                flat = flat * d.cells[a] + cell_index(d, a, xa);
+            }
         }
-    }
-    if (!AGG) {
-        if (!valid) return;
+        if (!AGG) {
+            if (valid) {
+                key[k] = flat;
+                atomicAdd(&count[flat], 1);
+            }
+            continue;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, valid ? flat : -1);
+        if (!valid) continue;
         key[k] = flat;
-        atomicAdd(&count[flat], 1);
-        return;
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[flat], __popc(peers));
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, valid ? flat : -1);
-    if (!valid) return;
-    key[k] = flat;
-    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[flat], __popc(peers));
 }
 
 // ---- exclusive scan of int32 (three-phase: tile scan, tile-sum scan, add) ----
@@ -198,19 +220,67 @@ __global__ void k_rank(long n, int ncells, const int* key, const int* start, con
     perm[st + rank] = k;
 }
 
+// fp16 layout length: cells padded to 32-slot blocks (only non-empty cells pad) + slack
+static long half_len(long n, long nc) { return ((n + 32L * std::min<long>(nc, n) + 64) + 7) & ~7L; }
+
+struct HalfOut {  // fp16 cell-relative coordinates of the padded layout (sweep.cuh HalfGrid)
+    __half* h;
+    long hlen;
+    const int* pstart;
+    int* escaped;
+};
+
+// Slot k (active, cell c, position x) into the padded fp16 layout; the cell's last
+// slot also writes the cell's +inf pads.
+template <int DIM>
+__device__ __forceinline__ void write_half(const DomainDev& d, const HalfOut& o, long k, int c,
+                                          const double* x, const int* cell_start,
+                                          const int* cell_count) {
+    const long rank = k - cell_start[c];
+    // 32-slot blocks, halves interleaved (sweep.cuh HalfGrid): rank -> word rank % 16
+    auto at = [&](long r) { return o.pstart[c] + (r & ~31L) + 2 * (r & 15) + ((r >> 4) & 1); };
+    const long p = at(rank);
+    int rem = c;
+    bool esc = false;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        const int ca = rem % d.cells[a];
+        rem /= d.cells[a];
+        const double q = (x[a] - d.lo[a]) / d.cs[a] - (double)ca;
+        // in its cell (floor == cell index) q lies in [0, 1): the fp16 bound of
+        // sweep.cuh HalfGrid assumes |h| <= 1; anything else disables the fp16 path
+        esc |= !(q >= 0.0 && q <= 1.0);
+        o.h[a * o.hlen + p] = __double2half(q);  // round to nearest
+    }
+    if (esc) atomicOr(o.escaped, 1);
+    if (rank == cell_count[c] - 1) {
+        const __half inf = __ushort_as_half((unsigned short)0x7c00);
+        const long re = (cell_count[c] + 31) & ~31;
+        for (long r = rank + 1; r < re; ++r)
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) o.h[a * o.hlen + at(r)] = inf;
+    }
+}
+
 struct ReorderTable {
     int nf;
+    unsigned long long skip;  // bit f: field f is written before it is read this step:
+                              // only inactive slots (whose values stay frozen) are moved
     int comps[kMaxFields];
     const double* src[kMaxFields];
     double* dst[kMaxFields];
 };
 
-// Also writes xl[s] = (float)(x - lo): global-origin fp32 coordinates, the
-// conservative pre-filter input of sweep.cuh / sweep_fast.cuh (NaN when inactive).
+// One gather pass per build: orig/key/active/skey, every field (minus `skip` for
+// active slots), the packed positions p4 (one 256-bit gather per pair in the
+// consumers), and when requested the fp32 pre-filter copy xl and the fp16
+// cell-relative coordinates of the list builder (no separate pass over r).
+template <int DIM>
 __global__ void k_reorder(DomainDev d, long n, const int* perm, const int* orig, const int* key,
                           const uint8_t* active, int* orig_s, int* key_s, uint8_t* active_s,
                           float4* xl, double4* p4, const int* skey, int* skey_s,
-                          ReorderTable t) {
+                          ReorderTable t, HalfOut ho, const int* cell_start,
+                          const int* cell_count) {
     long s = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (s >= n) return;
     int k = perm[s];
@@ -219,21 +289,28 @@ __global__ void k_reorder(DomainDev d, long n, const int* perm, const int* orig,
     skey_s[s] = skey[k];
     key_s[s] = kk;
     active_s[s] = active[k];
+    const bool act = kk < d.ncells;
     for (int f = 0; f < t.nf; ++f) {
+        if (act && ((t.skip >> f) & 1ULL)) continue;
         const double* src = t.src[f];
         double* dst = t.dst[f];
         for (int c = 0; c < t.comps[f]; ++c) dst[c * n + s] = src[c * n + k];
     }
-    float4 p = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
     double x[3] = {0.0, 0.0, 0.0};
-    for (int a = 0; a < d.dim; ++a) x[a] = t.src[0][a * n + k];
-    if (kk < d.ncells) {
-        float v[3] = {0.f, 0.f, 0.f};
-        for (int a = 0; a < d.dim; ++a) v[a] = (float)(x[a] - d.lo[a]);
-        p = make_float4(v[0], v[1], v[2], 0.f);
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) x[a] = t.src[0][a * n + k];
+    if (xl) {
+        float4 p = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
+        if (act) {
+            float v[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) v[a] = (float)(x[a] - d.lo[a]);
+            p = make_float4(v[0], v[1], v[2], 0.f);
+        }
+        xl[s] = p;
     }
-    xl[s] = p;
     p4[s] = make_double4(x[0], x[1], x[2], 0.0);
+    if (ho.h && act) write_half<DIM>(d, ho, s, kk, x, cell_start, cell_count);
 }
 
 template <int DIM>
@@ -309,34 +386,33 @@ __global__ void k_pcount(int nc, const int* count, int* pcount) {
 }
 
 __global__ void k_half_coords(DomainDev d, long n, const double* pos, const int* key,
-                              const int* cell_start, const int* cell_count, const int* pstart,
-                              long hlen, __half* h, int* escaped) {
+                              const int* cell_start, const int* cell_count, HalfOut o) {
     const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int c = key[k];
     if (c >= d.ncells) return;  // inactive tail
-    const long rank = k - cell_start[c];
-    // 32-slot blocks, halves interleaved (sweep.cuh HalfGrid): rank -> word rank % 16
-    auto at = [&](long r) { return pstart[c] + (r & ~31L) + 2 * (r & 15) + ((r >> 4) & 1); };
-    const long p = at(rank);
-    int rem = c;
-    bool esc = false;
-    for (int a = 0; a < d.dim; ++a) {
-        const int ca = rem % d.cells[a];
-        rem /= d.cells[a];
-        const double q = (pos[a * n + k] - d.lo[a]) / d.cs[a] - (double)ca;
-        // in its cell (floor == cell index) q lies in [0, 1): the fp16 bound of
-        // sweep.cuh HalfGrid assumes |h| <= 1; anything else disables the fp16 path
-        esc |= !(q >= 0.0 && q <= 1.0);
-        h[a * hlen + p] = __double2half(q);  // round to nearest
+    double x[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < d.dim; ++a) x[a] = pos[a * n + k];
+    if (d.dim == 3) write_half<3>(d, o, k, c, x, cell_start, cell_count);
+    else if (d.dim == 2) write_half<2>(d, o, k, c, x, cell_start, cell_count);
+    else write_half<1>(d, o, k, c, x, cell_start, cell_count);
+}
+
+// fp32 pre-filter coordinates xl[s] = (float)(x - lo) (NaN when inactive): the sweeps'
+// conservative pre-filter input. ONLY_ESCAPED: the fp16 list path's fallback, a no-op
+// unless some particle escaped its cell box.
+template <bool ONLY_ESCAPED>
+__global__ void k_xl(DomainDev d, long n, const double* pos, const int* key, float4* xl,
+                     const int* escaped) {
+    const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n || (ONLY_ESCAPED && *escaped == 0)) return;
+    float4 p = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
+    if (key[k] < d.ncells) {
+        float v[3] = {0.f, 0.f, 0.f};
+        for (int a = 0; a < d.dim; ++a) v[a] = (float)(pos[a * n + k] - d.lo[a]);
+        p = make_float4(v[0], v[1], v[2], 0.f);
     }
-    if (esc) atomicOr(escaped, 1);
-    if (rank == cell_count[c] - 1) {
-        const __half inf = __ushort_as_half((unsigned short)0x7c00);
-        const long re = (cell_count[c] + 31) & ~31;
-        for (long r = rank + 1; r < re; ++r)
-            for (int a = 0; a < d.dim; ++a) h[a * hlen + at(r)] = inf;
-    }
+    xl[k] = p;
 }
 
 __global__ void k_unsort(long n, int comps, const int* orig, const double* src, double* dst) {
@@ -378,11 +454,11 @@ void launch_build_cells(nau_ctx* c) {
     const bool agg = n >= 8L * nc;  // >= 8 particles per cell on average
     if (n > 0) {
         if (agg)
-            k_hash<true><<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_active,
+            k_hash<true><<<blocks_for(n, kBlock * kHashIlp), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_active,
                                                                   c->d_orig, c->d_key, c->d_cell_count,
                                                                   c->d_err);
         else
-            k_hash<false><<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_active,
+            k_hash<false><<<blocks_for(n, kBlock * kHashIlp), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_active,
                                                                    c->d_orig, c->d_key, c->d_cell_count,
                                                                    c->d_err);
         c->launches++;
@@ -404,16 +480,40 @@ void launch_build_cells(nau_ctx* c) {
     for (size_t f = 0; f < c->fields.size(); ++f) {
         FieldBuf& fb = c->fields[f];
         if (!fb.live) continue;
+        if ((c->reorder_skip >> f) & 1ULL) t.skip |= 1ULL << t.nf;
         t.comps[t.nf] = fb.comps();
         t.src[t.nf] = fb.d;
         t.dst[t.nf] = fb.alt;
         ++t.nf;
     }
-    k_reorder<<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->d_perm, c->d_orig, c->d_key,
-                                                       c->d_active, c->d_orig_s, c->d_key_s,
-                                                       c->d_active_s, c->d_xl, c->d_p4,
-                                                       c->d_skey, c->d_skey_s, t);
+    c->reorder_skip = 0;  // a hint for this build only
+    // the fp32 copy and the fp16 grid only when the last step read them
+    const bool want_xl = c->xl_used;
+    c->xl_used = false;
+    HalfOut ho{};
+    if (c->hq_used && c->d_hq && c->d_hesc && c->hq_len >= half_len(n, nc) &&
+        c->pstart_len >= nc + 1) {
+        k_pcount<<<blocks_for(nc + 1), kBlock, 0, c->stream>>>(nc, c->d_cell_count, c->d_pcount);
+        scan_exclusive(c, c->d_pcount, c->d_pstart, nc + 1);
+        cudaMemsetAsync(c->d_hesc, 0, sizeof(int), c->stream);
+        ho = HalfOut{c->d_hq, c->hq_len, c->d_pstart, c->d_hesc};
+        c->launches++;
+    }
+    c->hq_used = false;
+    auto reorder = [&](auto kern) {
+        kern<<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->d_perm, c->d_orig, c->d_key,
+                                                      c->d_active, c->d_orig_s, c->d_key_s,
+                                                      c->d_active_s, want_xl ? c->d_xl : nullptr,
+                                                      c->d_p4, c->d_skey, c->d_skey_s, t, ho,
+                                                      c->d_cell_start, c->d_cell_count);
+    };
+    if (c->dom.dim == 3) reorder(k_reorder<3>);
+    else if (c->dom.dim == 2) reorder(k_reorder<2>);
+    else reorder(k_reorder<1>);
     c->launches += 3;
+    // nau_build_cells increments rebuild_count after this: the copies belong to the next value
+    c->xl_rev = want_xl ? c->rebuild_count + 1 : -1;
+    c->hq_rev = ho.h ? c->rebuild_count + 1 : -1;
     std::swap(c->d_orig, c->d_orig_s);
     std::swap(c->d_skey, c->d_skey_s);
     std::swap(c->d_key, c->d_key_s);
@@ -422,9 +522,19 @@ void launch_build_cells(nau_ctx* c) {
         if (fb.live) std::swap(fb.d, fb.alt);
 }
 
+void ensure_xl(nau_ctx* c) {
+    c->xl_used = true;  // the next build writes it in its reorder pass
+    if (c->xl_rev == c->rebuild_count || c->n == 0) return;
+    k_xl<false><<<blocks_for(c->n), kBlock, 0, c->stream>>>(c->dom, c->n, c->fields[0].d,
+                                                            c->d_key, c->d_xl, nullptr);
+    c->launches++;
+    c->xl_rev = c->rebuild_count;
+}
+
 void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig) {
     cudaMemsetAsync(d_out_orig, 0, sizeof(int) * c->n, c->stream);
     if (c->n == 0) return;
+    ensure_xl(c);
     Geo g = make_geo(c);
     const int T = kSweepThreads;
     int b = blocks_for(c->n, T);
@@ -449,8 +559,7 @@ static HalfGrid half_grid(nau_ctx* c, double radius) {
     for (int a = 1; a < d.dim; ++a) iso &= d.cs[a] == d.cs[0];
     const double rho = radius / d.cs[0];
     if (!NAU_HALF || !iso || !(rho <= 1.5) || c->n == 0) return hg;
-    // cells padded to 32-slot blocks (only non-empty cells pad) plus slack
-    const long hlen = ((c->n + 32L * std::min<long>(nc, c->n) + 64) + 7) & ~7L;
+    const long hlen = half_len(c->n, nc);
     if (c->hq_len < hlen) {
         if (c->d_hq) cudaFree(c->d_hq);
         c->d_hq = nullptr;
@@ -481,11 +590,12 @@ static HalfGrid half_grid(nau_ctx* c, double radius) {
         scan_exclusive(c, c->d_pcount, c->d_pstart, nc + 1);
         cudaMemsetAsync(c->d_hesc, 0, sizeof(int), c->stream);
         k_half_coords<<<blocks_for(c->n), kBlock, 0, c->stream>>>(
-            d, c->n, c->fields[0].d, c->d_key, c->d_cell_start, c->d_cell_count, c->d_pstart,
-            c->hq_len, c->d_hq, c->d_hesc);
+            d, c->n, c->fields[0].d, c->d_key, c->d_cell_start, c->d_cell_count,
+            HalfOut{c->d_hq, c->hq_len, c->d_pstart, c->d_hesc});
         c->launches += 2;
         c->hq_rev = c->rebuild_count;
     }
+    c->hq_used = true;  // the next build writes the fp16 grid in its reorder pass
     for (int a = 0; a < 3; ++a) hg.h[a] = c->d_hq + a * c->hq_len;
     hg.pstart = c->d_pstart;
     hg.escaped = c->d_hesc;
@@ -523,6 +633,15 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs) {
     const int T = kSweepThreads;
     const int b = blocks_for(n, T);
     const HalfGrid hg = half_grid(c, radius);
+    if (!hg.on) {
+        ensure_xl(c);
+    } else if (c->xl_rev != c->rebuild_count) {
+        // the fp16 path falls back to the fp32 pre-filter when some particle escaped its
+        // cell box (a device flag): fill d_xl on the device in that case only
+        k_xl<true><<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_key,
+                                                             c->d_xl, c->d_hesc);
+        c->launches++;
+    }
     for (int attempt = 0; attempt < 3; ++attempt) {
         // uint2 records + two slack rows (consume_list reads two records ahead);
         // paired: uint4 records per thread pair + one slack row

@@ -328,7 +328,7 @@ static nau_status load_blocks(nau_ctx* c, SlabComm* s, const double* const* blk,
 nau_status nau_allreduce(nau_ctx* c, double* values, int count, int op) {
     if (!c || count < 0 || op < 0 || op > 2) return NAU_ERR_ARG;
     SlabComm* s = c->slab;
-    if (!s || s->nranks == 1 || count == 0) return NAU_OK;  // one rank: the local value
+    if (!s || count == 0) return NAU_OK;  // no communicator: the local value
     if (!nau::nccl().AllReduce) return comm_fail(c, NAU_ERR_COMM, "NCCL has no ncclAllReduce");
     if (s->red.reserve((size_t)count) != cudaSuccess)
         return comm_fail(c, NAU_ERR_CUDA, "allreduce: out of device memory");

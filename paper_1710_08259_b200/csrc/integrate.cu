@@ -23,6 +23,15 @@ constexpr int kBlock = 256;
 constexpr int kThreads = kSweepThreads;
 inline int blocks_for(long n, int b = kBlock) { return (int)((n + b - 1) / b); }
 
+// dst = src on active particles unless an error is latched (the fused sph_G11 + sph_L0
+// pass: the reference would not have evaluated the sph_L0 equation after a failure).
+__global__ void k_commit_if_ok(long n, const uint8_t* active, const double* src, double* dst,
+                               const DevErr* err) {
+    const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (k >= n || err->code != 0 || !active[k]) return;
+    dst[k] = src[k];
+}
+
 __global__ void k_euler(long n, int comps, const uint8_t* active, const int* orig, const double* x,
                         const double* xdot, double dt, double* out, DevErr* err) {
     long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
@@ -281,6 +290,12 @@ void wcsph_launch_dim(nau_ctx* c, const WcsphArgs& a, int kf) {
 
 }  // namespace
 
+void launch_commit_if_ok(nau_ctx* c, const double* src, double* dst) {
+    if (c->n == 0) return;
+    k_commit_if_ok<<<blocks_for(c->n), kBlock, 0, c->stream>>>(c->n, c->d_active, src, dst, c->d_err);
+    c->launches++;
+}
+
 void launch_euler(nau_ctx* c, const double* x, const double* xdot, double dt, double* out,
                   int comps) {
     if (c->n == 0) return;
@@ -305,6 +320,7 @@ void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p, bool lists) {
     a.nl = NList{lists ? c->d_nlist : nullptr, c->d_ncount, c->nl_cap};
     a.vp = c->d_aux;
     a.g = make_geo(c);
+    if (!lists) ensure_xl(c);
     a.xl = c->d_xl;
     a.mass = p->mass;
     a.radius = p->radius;

@@ -616,6 +616,7 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
     (void)out_cols;
     if (c->n == 0) return;
     const int dim = c->dom.dim;
+    if (op != NAU_OP_GRAVITY && !(op <= NAU_OP_SPH_A && lists)) ensure_xl(c);  // sweeps
     if (op <= NAU_OP_SPH_A) {
         SphArgs a;
         a.g = make_geo(c);

@@ -375,8 +375,12 @@ struct nau_ctx {
     int* d_pstart = nullptr;  // ncells + 1
     int* d_pcount = nullptr;  // ncells + 1 (rounded-up counts, scan input)
     long pstart_len = 0;
-    int* d_hesc = nullptr;    // escape flag
+    int* d_hesc = nullptr;    // escape flag (device)
     long hq_rev = -1;         // rebuild_count the fp16 copy belongs to
+    bool hq_used = false;     // the fp16 grid was used since the last build: k_reorder writes it
+    long xl_rev = -1;         // rebuild_count d_xl belongs to (ensure_xl)
+    bool xl_used = true;      // a sweep read d_xl since the last build: k_reorder writes it
+    unsigned long long reorder_skip = 0;  // fields the next build moves for inactive slots only
     // asynchronous host I/O (nau_upload_async / nau_download_async): one copy
     // stream per direction, per-field double-buffered staging in original order
     struct IoStage {
@@ -428,6 +432,9 @@ void prof_end(nau_ctx* c, int cls);
 // cells.cu
 void launch_boundary_shift(nau_ctx* c);
 void launch_build_cells(nau_ctx* c);
+// d_xl (fp32 pre-filter coordinates) valid for the current cell build; every launch
+// that may sweep calls this (the paired fp16 list path does not read d_xl).
+void ensure_xl(nau_ctx* c);
 void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig);
 bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs = false);  // false: unusable
 // The current cell build's list for (radius, order, layout), built on first use
@@ -446,6 +453,7 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
                      const double* gadd = nullptr, const GravSources* gsrc = nullptr,
                      bool lists = false);
 // integrate.cu
+void launch_commit_if_ok(nau_ctx* c, const double* src, double* dst);
 void launch_euler(nau_ctx* c, const double* x, const double* xdot, double dt, double* out,
                   int comps);
 void launch_symplectic(nau_ctx* c, double* v, const double* vdot, const double* mask, double dt);

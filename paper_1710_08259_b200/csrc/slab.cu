@@ -250,6 +250,7 @@ nau_status nau_load_rows(nau_ctx* c, const double* dev_rows, long m, int gid_fie
     c->built_once = false;
     c->nl_rev = -1;
     c->hq_rev = -1;
+    c->xl_rev = -1;
     return NAU_OK;
 }
 

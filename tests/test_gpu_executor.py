@@ -168,3 +168,46 @@ def test_executor_equals_the_fused_deck():
             ctx.close()
     for k in out[0]:
         assert rel_err(out[1][k], out[0][k]) <= 1e-12, k  # Tait pow: device vs host libm
+
+
+@pytest.mark.parametrize("deck", ["cahn_hilliard_patch", "particle_damper"])
+def test_reductions_through_a_communicator(deck):
+    """With a communicator attached (nau_comm_init), every reduction of the executor goes
+    through ncclAllReduce (nau_allreduce: the §8(e) reduction over slab ranks): on a
+    1-rank communicator the decks' fmax -> dt and fsum -> F results equal the run without
+    one bitwise."""
+    meta = json.loads(str(Z[f"{deck}_meta"]))
+    runs = []
+    for comm in (False, True):
+        ctx, cs = build(deck, meta)
+        try:
+            if comm:
+                ctx.comm_init(nau.Context.comm_unique_id(), 1, 0)
+            for name, text in meta["equations"]:
+                cs.equation(name, text)
+            for _ in range(3):
+                cs.solve_step()
+            runs.append({vn: cs.get_variable(vn) for vn, _ in meta["variables"]})
+        finally:
+            ctx.close()
+    for vn in runs[0]:
+        np.testing.assert_array_equal(runs[1][vn], runs[0][vn], err_msg=vn)
+
+
+def test_allreduce_ops_on_one_rank():
+    ctx = nau.Context(0)
+    try:
+        ctx.set_domain(1, [0], [1], [1.0], [nau.CUTOFF])
+        ctx.set_particles(np.array([[0.5]]))
+        L = ctx.L
+        v = np.array([1.5, -2.0, 3.0])
+        assert L.nau_comm_size(ctx.h) == 1
+        assert L.nau_allreduce(ctx.h, v.ctypes.data_as(nau.C.c_void_p), 3, 0) == 0  # no comm
+        ctx.comm_init(nau.Context.comm_unique_id(), 1, 0)
+        for op in (0, 1, 2):
+            w = v.copy()
+            assert L.nau_allreduce(ctx.h, w.ctypes.data_as(nau.C.c_void_p), 3, op) == 0
+            np.testing.assert_array_equal(w, v)
+        assert L.nau_allreduce(ctx.h, v.ctypes.data_as(nau.C.c_void_p), 3, 7) != 0
+    finally:
+        ctx.close()

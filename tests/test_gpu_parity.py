@@ -486,6 +486,8 @@ def test_fused_g11_l0_errors_like_two_calls():
                 c.interact("sph_L0", ["A", 0.5, "rho", 0.3], "L", kernel="Wp53220")
             c.sync()
         msgs.append(str(ei.value))
+        if fused:  # the reference never evaluates the sph_L0 equation: L keeps its values
+            assert not np.any(c.download("L"))
         c.close()
     assert msgs[0] == msgs[1] and msgs[0]
     spec["fields"]["rho"][0, 123] = 1000.0
