@@ -616,7 +616,10 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
     (void)out_cols;
     if (c->n == 0) return;
     const int dim = c->dom.dim;
-    if (op != NAU_OP_GRAVITY && !(op <= NAU_OP_SPH_A && lists)) ensure_xl(c);  // sweeps
+    // every path that sweeps reads the fp32 pre-filter copy (sph_launch: a tensor-valued
+    // sph_S operand sweeps even when a list exists)
+    const bool list_path = op <= NAU_OP_SPH_A && lists && !(op == NAU_OP_SPH_S && a_rows * a_cols > 1);
+    if (op != NAU_OP_GRAVITY && !list_path) ensure_xl(c);
     if (op <= NAU_OP_SPH_A) {
         SphArgs a;
         a.g = make_geo(c);
