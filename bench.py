@@ -214,8 +214,8 @@ WORKLOAD_NAMES = {
     0: "cfg0: 2D WCSPH dam break, 20,000 fluid + 3-layer walls, dx=0.01",
     1: "cfg1: 3D SPH operator microbench, N=1,048,576 periodic, cubic spline",
     2: "cfg2: 3D WCSPH dam break, 4.0M fluid + 3-layer walls, dx=0.005, Wendland C2",
-    3: ("cfg3: 3D DEM granular settling, 2,000,000 spheres, log-normal radii, "
-        "linear spring-dashpot + Coulomb, dt=1e-6"),
+    3: ("cfg3: 3D DEM granular settling, 2,000,000 spheres, untruncated log-normal radii at "
+        "seeded random-sequential-addition positions, linear spring-dashpot + Coulomb, dt=1e-6"),
     4: "cfg4: 3D n-body Plummer sphere, N=262,144, eps=0.01, leapfrog dt=1e-3",
 }
 

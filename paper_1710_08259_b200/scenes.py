@@ -144,30 +144,52 @@ def dam_break(dim=2, dx=0.01, fluid=None, tank=None, layers=3, rho0=1000.0, grav
 
 
 # ---------------------------------------------------------------- cfg3 ----
-def dem_column(n=2_000_000, seed=3, box=(0.3, 0.3, 1.2), median=1e-3, sigma=0.2,
-               rho_s=2500.0, kn=1e5, en=0.5, mu=0.5, dt=1e-6, gravity=9.81) -> Scene:
-    """BASELINE cfg3: n spheres, log-normal radii (median, sigma_log) from Box-Muller on
-    draws 0,1 of the reference RNG, settling under gravity in a column with
-    symmetric (mirror-image) walls — the floor is the z-low wall
-    (interactions.cpp:168-170 mirror mechanism). Linear spring-dashpot normal force
-    k_n, restitution e_n, Coulomb friction mu; cell = search radius = 2 r_max.
+def _rsa_place(R, box, seed, max_tries=100000):
+    """Seeded random sequential addition (csrc/scenes_rsa.c, libnau_scenes.so): sphere s
+    in index order, attempt t at a uniform centre in [R_s, box - R_s] drawn with the
+    reference's counter RNG (seed + 1 + t, particle s, draws 0-2), accepted when it
+    overlaps no earlier sphere (hash grid of cell 2 max R)."""
+    import ctypes as C
+    import os
+    lib = C.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnau_scenes.so"))
+    lib.nau_rsa_place.restype = C.c_long
+    lib.nau_rsa_place.argtypes = [C.c_long, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p]
+    R = np.ascontiguousarray(R, np.float64)
+    b = np.ascontiguousarray(box, np.float64)
+    pos = np.zeros((3, len(R)))
+    rc = lib.nau_rsa_place(len(R), R.ctypes.data, b.ctypes.data, seed, max_tries, pos.ctypes.data)
+    if rc:
+        raise RuntimeError(f"random sequential addition: sphere {rc - 1} unplaced")
+    return pos
 
-    Stand-in for random sequential addition: a jittered cubic lattice with the
-    same number density; radii are clamped at 0.95 s/2 (s = lattice spacing,
-    about +3 sigma; 0.1% of the draws) so the jittered lattice never overlaps.
-    """
+
+def dem_column(n=2_000_000, seed=3, box=(0.3, 0.3, 1.2), median=1e-3, sigma=0.2,
+               rho_s=2500.0, kn=1e5, en=0.5, mu=0.5, dt=1e-6, gravity=9.81,
+               placement="rsa") -> Scene:
+    """BASELINE cfg3: n spheres, log-normal radii (median, sigma_log; untruncated) from
+    Box-Muller on draws 0,1 of the reference RNG, at seeded random-sequential-addition
+    positions (non-overlapping, _rsa_place) in the column, settling under gravity with
+    symmetric (mirror-image) walls — the floor is the z-low wall (interactions.cpp:168-170
+    mirror mechanism). Linear spring-dashpot normal force k_n, restitution e_n, Coulomb
+    friction mu; cell = search radius = 2 r_max (the largest realised radius).
+    placement="lattice": the round-1 jittered cubic lattice (radii clamped at 0.95 s/2)."""
     d = uniform_draws(seed, n, 5)
     u1 = np.maximum(d[0], 2.0 ** -53)
     z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * math.pi * d[1])
-    s = (box[0] * box[1] * box[2] / n) ** (1.0 / 3.0)
-    nx, ny = int(box[0] / s), int(box[1] / s)
-    nz = int(math.ceil(n / (nx * ny)))
-    s = min(box[0] / nx, box[1] / ny, box[2] / nz)
-    R = np.minimum(median * np.exp(sigma * z), 0.95 * 0.5 * s)
-    k = np.arange(n)
-    site = np.stack([(k % nx + 0.5) * s, ((k // nx) % ny + 0.5) * s, (k // (nx * ny) + 0.5) * s])
-    room = 0.5 * s - R  # jitter keeps every sphere inside its lattice cube
-    pos = np.ascontiguousarray(site + (2.0 * d[2:5] - 1.0) * room * 0.999)
+    R = median * np.exp(sigma * z)
+    if placement == "rsa":
+        pos = np.ascontiguousarray(_rsa_place(R, box, seed))
+        s = None
+    else:
+        s = (box[0] * box[1] * box[2] / n) ** (1.0 / 3.0)
+        nx, ny = int(box[0] / s), int(box[1] / s)
+        nz = int(math.ceil(n / (nx * ny)))
+        s = min(box[0] / nx, box[1] / ny, box[2] / nz)
+        R = np.minimum(R, 0.95 * 0.5 * s)
+        k = np.arange(n)
+        site = np.stack([(k % nx + 0.5) * s, ((k // nx) % ny + 0.5) * s, (k // (nx * ny) + 0.5) * s])
+        room = 0.5 * s - R  # jitter keeps every sphere inside its lattice cube
+        pos = np.ascontiguousarray(site + (2.0 * d[2:5] - 1.0) * room * 0.999)
     rmax = float(R.max())
     cs = 2.0 * rmax
     cells = [int(math.ceil(b / cs)) for b in box]
@@ -175,7 +197,8 @@ def dem_column(n=2_000_000, seed=3, box=(0.3, 0.3, 1.2), median=1e-3, sigma=0.2,
     return Scene("dem_column", 3, [0, 0, 0], cells, [cs] * 3, [1, 1, 1], pos,
                  fields={"v": np.zeros((3, n)), "vdot": np.zeros((3, n)), "R": R, "m": m},
                  params={"kn": kn, "en": en, "cf": mu, "dt": dt, "g": [0.0, 0.0, -gravity],
-                         "search_radius": cs, "rho_s": rho_s, "lattice": s})
+                         "search_radius": cs, "rho_s": rho_s, "lattice": s,
+                         "placement": placement})
 
 
 def dem_equations():
