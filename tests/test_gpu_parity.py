@@ -1011,7 +1011,7 @@ def _dem_port_step(ps, st, prm, R, m):
 def test_dem_deck_vs_port(ctx, fast):
     """cfg3 deck on a small compressed column (many contacts, floor via mirror images):
     EXACT mode bitwise (no libm transcendental in the linear law); FAST within 1e-10."""
-    sc = scenes.dem_column(n=6000, box=(0.03, 0.03, 0.06), dt=1e-5)
+    sc = scenes.dem_column(n=6000, box=(0.03, 0.03, 0.06), dt=1e-5, placement="lattice")
     prm = sc.params
     sc.pos[2] *= 0.6  # squeeze the column vertically: overlapping contacts from step 1
     sc.fields["v"][:] = np.random.default_rng(3).uniform(-0.05, 0.05, (3, sc.n))
