@@ -571,39 +571,107 @@ class GravityShard(Gravity):
         return c
 
 
-class DamBreakSlab(DamBreak):
-    """cfg2/cfg0 slab-decomposed along x over the ranks (paper_1710_08259_b200/slab.py):
-    each rank owns whole x-cell planes (balanced on particle counts) plus two ghost
-    planes per face; migration + ghost refresh over NCCL every step."""
+class _SlabMixin:
+    """Common setup of the slab-decomposed decks (paper_1710_08259_b200/slab.py, SURVEY.md
+    §8(e)): x-threshold slabs balanced on a fine x-histogram, owned particles + the
+    ghosts within one interaction radius of each face; the local set is rebuilt in place
+    each step (no full reload); the torch driver re-balances every 100 steps."""
+
+    REBALANCE_EVERY = 100
+
+    def _slab_setup(self, ctx, radius, field_widths):
+        import torch
+        from paper_1710_08259_b200 import nau, slab
+        sc = self.sc
+        self.periodic = sc.kinds[0] == 0
+        lo = sc.min_cells[0] * sc.cell_size[0]
+        hi = sc.max_cells[0] * sc.cell_size[0]
+        world, rank = self.dist.world, self.dist.rank
+        self.R = radius
+        self.bounds = slab.balanced_x_bounds(sc.pos[0], lo, hi, world, 2.0 * radius)
+        names = [k for k, _ in field_widths]
+        rows = slab.initial_rows(sc, names, self.bounds, rank, radius, self.periodic)
+        d = sc.dim
+        ctx.set_domain(sc.dim, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+        ctx.set_particles(np.ascontiguousarray(rows[:, :d].T))
+        for k, w in field_widths + [("gid", 1), ("ghost", 1)]:
+            ctx.add_field(k, w, 1, 0.0)
+        # room for arrivals: ghosts and immigrants of later steps (rebuilt in place)
+        ctx._check(ctx.L.nau_reserve(ctx.h, int(1.25 * len(rows)) + 65536))
+        self.rows0 = rows
+        return rows
+
+    def _slab_driver(self, ctx, backend):
+        import torch
+        from paper_1710_08259_b200 import nau, slab
+        world, rank = self.dist.world, self.dist.rank
+        self.backend = backend
+        backend.load(torch.from_numpy(self.rows0).to(backend.device))
+        if self.native:
+            uid = [nau.Context.comm_unique_id() if rank == 0 else None]
+            if world > 1:
+                self.dist.pg.broadcast_object_list(uid, src=0)
+            ctx.comm_init(uid[0], world, rank)
+            ctx.slab_config(0, self.bounds, self.periodic, self.R)
+            self.rank_drv = None
+        else:
+            ex = slab.Exchanger(self.dist.pg, rank, world, self.periodic, backend.device)
+            self.rank_drv = slab.SlabRank(backend, ex, self.bounds, self.R, self.periodic,
+                                          rebalance_every=self.REBALANCE_EVERY)
+        self.steps_done = 0
+        self.n_active = int((self.rows0[:, -1] == 0).sum())
+        self.h_rows = torch.from_numpy(self.rows0).pin_memory()
+        self.h_out = torch.empty_like(self.h_rows).pin_memory()
+        self.h2d = self.d2h = self.h_rows.numel() * 8
+
+    def _native_exchange(self, ctx):
+        """Migration + halo after the integrator; re-balancing every 100 steps (comm.cu)."""
+        if self.dist.world == 1:
+            return
+        self.steps_done += 1
+        if self.steps_done % self.REBALANCE_EVERY == 0:
+            ctx.slab_rebalance()
+        else:
+            ctx.migrate()
+
+    def e2e_step(self, ctx):
+        import torch
+        from paper_1710_08259_b200 import slab
+        dev_rows = self.h_rows.to(self.backend.device, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        self.backend.load(dev_rows)
+        self.step(ctx)
+        local = self.backend.pack(self.backend.select_x(-math.inf, math.inf, slab.FLAG_OWNED,
+                                                        slab.FLAG_OWNED))
+        m = min(local.shape[0], self.h_out.shape[0])
+        self.h_out[:m].copy_(local[:m], non_blocking=False)
+
+    def slab_config(self):
+        drv = self.rank_drv
+        return {"slabs_x": [round(b, 6) for b in (drv.bounds if drv else self.bounds)],
+                "halo": f"ghosts within R = {self.R:.6g} of each face (not evaluated)",
+                "rebalance_every": self.REBALANCE_EVERY,
+                "exchange": ("native NCCL (comm.cu)" if self.native
+                             else "torch.distributed (slab.py)")}
+
+
+class DamBreakSlab(_SlabMixin, DamBreak):
+    """cfg2/cfg0 slab-decomposed along x: per step density pass, halo values (rho, p) to
+    the ghosts, momentum pass, integrator, then migration + halo in one exchange."""
 
     FIELDS = ["rho", "p", "v", "vdot", "mask"]
 
     def __init__(self, dim, dist, native=False):
         super().__init__(dim)
         self.dist = dist
-        self.native = native  # exchange through the library's own NCCL layer (comm.cu)
+        self.native = native
 
     def setup(self, ctx):
-        import torch
         from paper_1710_08259_b200 import nau, slab
         sc, prm = self.sc, self.sc.params
-        periodic = sc.kinds[0] == 0
-        ncx = sc.max_cells[0] - sc.min_cells[0]
-        lo, cs = sc.min_cells[0] * sc.cell_size[0], sc.cell_size[0]
-        cx = slab.cell_x_of(sc.pos[0], lo, cs, ncx, periodic)
-        world, rank = self.dist.world, self.dist.rank
-        self.bounds = slab.balanced_bounds(cx, ncx, world)
-        rows = slab.initial_rows(sc, self.FIELDS, self.bounds, rank, ncx, periodic)
         d = sc.dim
-        ctx.set_domain(sc.dim, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
-        ctx.set_particles(np.ascontiguousarray(rows[:, :d].T))
-        col = d
-        for k in self.FIELDS + ["gid", "ghost"]:
-            w = d if k in ("v", "vdot") else 1
-            ctx.add_field(k, w, 1, np.ascontiguousarray(rows[:, col:col + w].T))
-            col += w
-        ctx.boundary_shift()
-        ctx.build_cells()
+        self._slab_setup(ctx, prm["radius"], [("rho", 1), ("p", 1), ("v", d), ("vdot", d),
+                                              ("mask", 1)])
         p = nau.WcsphParams()
         p.kernel_family, p.kernel_dim = nau.K_WENDLAND, sc.dim
         p.mass, p.radius, p.rho0, p.B = prm["mass"], prm["radius"], prm["rho0"], prm["B"]
@@ -614,93 +682,57 @@ class DamBreakSlab(DamBreak):
         p.f_rho, p.f_p, p.f_v, p.f_vdot, p.f_mask = (f["rho"].id, f["p"].id, f["v"].id,
                                                      f["vdot"].id, f["mask"].id)
         self.p = p
-        self.backend = slab.GpuBackend(ctx, p, self.FIELDS)
-        dev = self.backend.device
-        ex = slab.Exchanger(self.dist.pg, rank, world, periodic, dev)
-        # torch driver: re-balance the slab bounds every 100 steps
-        self.rank_drv = slab.SlabRank(self.backend, ex, self.bounds, ncx, periodic,
-                                      rebalance_every=0 if self.native else 100, x_lo=lo,
-                                      cell_size=cs)
-        if self.native:
-            uid = [nau.Context.comm_unique_id() if rank == 0 else None]
-            if world > 1:
-                self.dist.pg.broadcast_object_list(uid, src=0)
-            ctx.comm_init(uid[0], world, rank)
-            ctx.slab_config(0, self.bounds, periodic, slab.SlabRank.GHOST_PLANES)
-        self.n_active = int((rows[:, -1] == 0).sum())
-        N = float(len(rows))
+        self._slab_driver(ctx, slab.GpuBackend(ctx, p))
+        N = float(len(self.rows0))
         self.kernels = {
             200: ("density+EOS", (8.0 * d + 8 + 8) * N, 0.0),
             201: ("momentum G11+A", (8.0 * d * 3 + 16) * N, 0.0),
-            302: ("neighbour-list build", 20.0 * N, 0.0),
+            302: ("neighbour-list build", 8.0 * d * N, 0.0),
             301: ("symplectic integrator", (8.0 * (4 * d + 1) + 8 * 2 * d) * N, 20.0 * N),
-            300: ("cell build", (8.0 * d + 8 + 60 + 4 + 16 * (3 * d + 5)) * N, 0.0),
+            300: ("cell build", (8.0 * d + 8 + 60 + 4 + 16 * (2 * d + 4)) * N, 0.0),
         }
         self.survey = None  # per-rank slabs: C and n are not counted
         self.cand_per_particle = float("nan")
         self.nbr_per_particle = float("nan")
-        self.h_rows = torch.from_numpy(rows).pin_memory()
-        self.h_out = torch.empty_like(self.h_rows).pin_memory()
-        self.h2d = self.h_rows.numel() * 8
-        self.d2h = self.h_rows.numel() * 8
 
     def step(self, ctx):
-        if self.native:  # nau_wcsph_step; nau_migrate; nau_halo_exchange (comm.cu)
-            ctx.wcsph_step(self.p)
-            ctx.migrate()
-            ctx.halo_exchange()
-        else:
+        if not self.native:
             self.rank_drv.step()
-
-    def e2e_step(self, ctx):
-        import torch
-        dev_rows = self.h_rows.to(self.backend.device, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        self.backend.load(dev_rows)
-        self.step(ctx)
-        local = self.backend.select(-(1 << 30), 1 << 30, 0)
-        m = min(local.shape[0], self.h_out.shape[0])
-        self.h_out[:m].copy_(local[:m], non_blocking=False)
+            return
+        if self.dist.world == 1:
+            ctx.wcsph_step(self.p)
+            return
+        import ctypes as C
+        ctx.wcsph_pass(self.p, 0)
+        ctx.halo_exchange(["rho", "p"])
+        ctx._check(ctx.L.nau_wcsph_ghost_payload(ctx.h, C.byref(self.p)))
+        ctx.wcsph_pass(self.p, 1)
+        ctx.wcsph_pass(self.p, 2)
+        self._native_exchange(ctx)
 
     def config(self):
         c = super().config()
         c.pop("candidates_per_particle", None)
         c.pop("neighbours_per_particle", None)
-        c["slabs"] = self.bounds
-        c["ghost_planes"] = 2
-        c["rebalance_every"] = self.rank_drv.rebalance_every
-        c["exchange"] = "native NCCL (comm.cu)" if self.native else "torch.distributed (slab.py)"
+        c.update(self.slab_config())
         return c
 
 
-class DemSlab(DemColumn):
-    """cfg3 slab-decomposed along x (0.3 m ≈ 85 planes, balanced while
-    the column settles in z); same slab driver as the dam break, DEM deck step."""
+class DemSlab(_SlabMixin, DemColumn):
+    """cfg3 slab-decomposed along x (balanced while the column settles
+    in z); the DEM deck is one neighbour pass, so only migration + halo per step."""
 
     FIELDS = ["v", "vdot", "R", "m"]
 
-    def __init__(self, dist):
+    def __init__(self, dist, native=False):
         super().__init__()
         self.dist = dist
+        self.native = native
 
     def setup(self, ctx):
-        import torch
         from paper_1710_08259_b200 import nau, slab
         sc, prm = self.sc, self.sc.params
-        ncx = sc.max_cells[0] - sc.min_cells[0]
-        cx = slab.cell_x_of(sc.pos[0], 0.0, sc.cell_size[0], ncx, False)
-        world, rank = self.dist.world, self.dist.rank
-        self.bounds = slab.balanced_bounds(cx, ncx, world)
-        rows = slab.initial_rows(sc, self.FIELDS, self.bounds, rank, ncx, False)
-        ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
-        ctx.set_particles(np.ascontiguousarray(rows[:, :3].T))
-        col = 3
-        for k in self.FIELDS + ["gid", "ghost"]:
-            w = 3 if k in ("v", "vdot") else 1
-            ctx.add_field(k, w, 1, np.ascontiguousarray(rows[:, col:col + w].T))
-            col += w
-        ctx.boundary_shift()
-        ctx.build_cells()
+        self._slab_setup(ctx, prm["search_radius"], [("v", 3), ("vdot", 3), ("R", 1), ("m", 1)])
         p = nau.DemParams()
         f = ctx.fields
         p.law, p.f_v, p.f_vdot, p.f_R, p.f_m = 8, f["v"].id, f["vdot"].id, f["R"].id, f["m"].id
@@ -709,29 +741,25 @@ class DemSlab(DemColumn):
         for a in range(3):
             p.g[a] = prm["g"][a]
         self.p = p
-        self.backend = slab.GpuBackend(ctx, lambda: ctx.dem_step(p), self.FIELDS)
-        ex = slab.Exchanger(self.dist.pg, rank, world, False, self.backend.device)
-        self.rank_drv = slab.SlabRank(self.backend, ex, self.bounds, ncx, False)
-        self.n_active = int((rows[:, -1] == 0).sum())
-        N = float(len(rows))
+        self._slab_driver(ctx, slab.GpuBackend(ctx, None, step_fn=lambda: ctx.dem_step(p)))
+        N = float(len(self.rows0))
         self.kernels = {108: ("dem_lsd contact sum", 88.0 * N, 0.0),
-                        301: ("symplectic integrator", 8.0 * 22 * N, 20.0 * N),
-                        300: ("cell build", (24.0 + 8 + 60 + 4 + 16 * 13) * N, 0.0)}
+                        301: ("symplectic integrator", 8.0 * 15 * N, 20.0 * N),
+                        300: ("cell build", (24.0 + 8 + 60 + 4 + 16 * 10) * N, 0.0)}
         self.cand_per_particle = float("nan")
-        self.h_rows = torch.from_numpy(rows).pin_memory()
-        self.h_out = torch.empty_like(self.h_rows).pin_memory()
-        self.h2d = self.d2h = self.h_rows.numel() * 8
 
     def step(self, ctx):
-        self.rank_drv.step()
-
-    def e2e_step(self, ctx):
-        DamBreakSlab.e2e_step(self, ctx)
+        if self.native:
+            ctx.dem_step(self.p)
+            self._native_exchange(ctx)
+        else:
+            self.rank_drv.step()
 
     def config(self):
         sc = self.sc
-        return {"workload": self.name, "particles": sc.n, "dt": sc.params["dt"],
-                "slabs": self.bounds, "ghost_planes": 2}
+        c = {"workload": self.name, "particles": sc.n, "dt": sc.params["dt"]}
+        c.update(self.slab_config())
+        return c
 
 
 def make_workload(cfg, dist=None, slab=False, native=False):
@@ -740,7 +768,7 @@ def make_workload(cfg, dist=None, slab=False, native=False):
     if slab and cfg == 4:
         return GravityShard(dist)
     if slab and cfg == 3:
-        return DemSlab(dist)
+        return DemSlab(dist, native)
     return {1: Microbench, 2: lambda: DamBreak(3), 0: lambda: DamBreak(2), 3: DemColumn,
             4: Gravity}[cfg]()
 

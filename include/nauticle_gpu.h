@@ -213,6 +213,10 @@ typedef struct {
     int f_rho, f_p, f_v, f_vdot, f_mask;
 } nau_wcsph_params;
 nau_status nau_wcsph_step(nau_ctx* ctx, const nau_wcsph_params* prm);
+/* The step's passes one at a time (multi-GPU slabs exchange halo values between
+ * them): 0 = cell build + neighbour list + density/EOS, 1 = momentum
+ * (after pass 0 of the same build), 2 = symplectic update + boundary shift. */
+nau_status nau_wcsph_pass(nau_ctx* ctx, const nau_wcsph_params* prm, int pass);
 
 /* DEM deck (BASELINE cfg3), the reference's equation form:
  *   vdot = law(v, R, P, Q, m, cf, Rs) + g;  v = euler(v, vdot, dt);  r = euler(r, v, dt)
@@ -351,6 +355,33 @@ nau_status nau_pack_rows(nau_ctx* ctx, const int* dev_slots, long m, double* dev
  * field holding global particle indices: cells then list particles in ascending
  * global index, so sums keep the single-GPU order. Marks cells dirty. */
 nau_status nau_load_rows(nau_ctx* ctx, const double* dev_rows, long m, int gid_field);
+/* x-threshold slabs (slab.py): slots of active particles with coordinate `axis` in
+ * [xlo, xhi) and flag in [flag_lo, flag_hi], ascending slot order. Syncs. */
+nau_status nau_select_x(nau_ctx* ctx, int axis, double xlo, double xhi, int flag_field,
+                        double flag_lo, double flag_hi, int* dev_slots, long* count);
+/* Capacity for up to `cap` particles (before loading: contents are dropped). */
+nau_status nau_reserve(nau_ctx* ctx, long cap);
+/* In place: the particle set becomes the kept slots (in the given order) followed by
+ * m_new rows (nau_row_width layout, gid_field as in nau_load_rows); one pass over the
+ * kept particles. Marks cells dirty. */
+nau_status nau_rebuild_rows(nau_ctx* ctx, const int* dev_keep, long m_keep,
+                            const double* dev_rows, long m_new, int gid_field);
+/* Per-bin counts (device, unsigned 64-bit) of active particles with coordinate `axis`
+ * in nbins equal bins over [x0, x1) (clamped), flag in [flag_lo, flag_hi]. */
+nau_status nau_histogram_x(nau_ctx* ctx, int axis, double x0, double x1, int nbins,
+                           int flag_field, double flag_lo, double flag_hi,
+                           unsigned long long* dev_counts);
+/* Ghosts: particles whose scalar field `field_id` is non-zero take part in every sum
+ * as neighbours but are not evaluated or integrated (their values come from the rank
+ * that owns them); -1 switches this off. */
+nau_status nau_set_ghost_field(nau_ctx* ctx, int field_id);
+/* Halo values of the WCSPH deck between its passes (the Python driver): (rho, p) rows
+ * of the given slots, and back into ghost slots with the momentum payload
+ * (v, p / rho^2) they imply. */
+nau_status nau_wcsph_pack_rho_p(nau_ctx* ctx, const nau_wcsph_params* prm, const int* dev_slots,
+                                long m, double* dev_rows);
+nau_status nau_wcsph_ghost_update(nau_ctx* ctx, const nau_wcsph_params* prm, const int* dev_slots,
+                                  long m, const double* dev_rows);
 
 /* ---- native slab exchange over NCCL (nau_comm_init /
  * nau_halo_exchange / nau_migrate; comm.cu). One context per GPU and process;
@@ -360,29 +391,46 @@ nau_status nau_load_rows(nau_ctx* ctx, const double* dev_rows, long m, int gid_f
 nau_status nau_comm_unique_id(unsigned char* id_out /* NAU_COMM_ID_BYTES */);
 nau_status nau_comm_init(nau_ctx* ctx, const unsigned char* id, int nranks, int rank);
 void nau_comm_destroy(nau_ctx* ctx);
-/* Rank r owns cells [bounds[r], bounds[r+1]) along `axis` (bounds: nranks + 1
- * cell-plane indices from 0 to the cell count) plus ghost copies of the
- * `ghost_planes` planes beyond each face; gid_field / ghost_field are scalar
- * fields holding the global index (the within-cell sort key) and the ghost flag. */
-nau_status nau_slab_config(nau_ctx* ctx, int axis, const int* bounds, int periodic,
-                           int ghost_planes, int gid_field, int ghost_field);
-/* Owned particles whose cell left the slab move to the owning neighbour; the
- * context then holds its owned particles only. Syncs. */
+/* x-threshold slabs: rank r owns the particles with coordinate
+ * `axis` in [bounds[r], bounds[r+1]) (nranks + 1 values from the domain's lo to hi,
+ * every slab at least 2 radius wide) and holds ghosts: its neighbours' particles within
+ * `radius` of its faces, flag_field 1 (owned by the left neighbour) or 2 (right), which
+ * take part in every sum but are not evaluated or integrated (nau_set_ghost_field).
+ * gid_field holds global indices (the within-cell sort key). */
+nau_status nau_slab_config(nau_ctx* ctx, int axis, const double* bounds, int periodic,
+                           double radius, int gid_field, int flag_field);
+nau_status nau_slab_bounds(nau_ctx* ctx, double* bounds_out /* nranks + 1 */);
+/* Migration + halo after the integrator, one exchange round: owned particles that left
+ * the slab go to the neighbour (less than radius past the face, else NAU_ERR_COMM),
+ * owned particles within radius of a face go to that neighbour as ghosts, emigrants
+ * stay as ghosts of their new owner; the local set is rebuilt in place. Syncs. */
 nau_status nau_migrate(nau_ctx* ctx);
-/* The first / last ghost_planes owned planes go to the neighbours; the context
- * then holds owned + ghost particles (ghost flag 1). Syncs. */
-nau_status nau_halo_exchange(nau_ctx* ctx);
+/* Halo values between passes: the listed fields of every owned particle within radius
+ * of a face to that neighbour, into its ghosts of that face (same slot order on both
+ * sides: the global cell grid ordered by global id). Syncs. */
+nau_status nau_halo_exchange(nau_ctx* ctx, const int* field_ids, int nfields);
+/* Re-balancing: bounds from the all-reduced nbins-bin x-histogram of owned particles,
+ * owned particles hop to their new owner, then a new halo. Syncs. */
+nau_status nau_slab_rebalance(nau_ctx* ctx, int nbins);
+/* Field subsets of selected slots as rows (width = the fields' components) and back. */
+nau_status nau_pack_fields(nau_ctx* ctx, const int* dev_slots, long m, const int* field_ids,
+                           int nfields, double* dev_rows);
+nau_status nau_unpack_fields(nau_ctx* ctx, const int* dev_slots, long m, const int* field_ids,
+                             int nfields, const double* dev_rows);
+/* The WCSPH momentum payload (v, p / rho^2) of every ghost from its fields (after a
+ * nau_halo_exchange of rho and p). */
+nau_status nau_wcsph_ghost_payload(nau_ctx* ctx, const nau_wcsph_params* prm);
+/* The primitive under both: swap device row blocks (width doubles per row) with
+ * the left / right neighbours; received blocks stay valid until the next call. */
+nau_status nau_comm_swap(nau_ctx* ctx, const double* to_left, long n_left, const double* to_right,
+                         long n_right, int width, const double** from_left, long* nf_left,
+                         const double** from_right, long* nf_right);
 /* ≙ the ncclAllReduce of SURVEY.md §8(e) "Reductions": host values combined over the
  * ranks of the context's communicator (op 0 sum, 1 max, 2 min), in place. Without a
  * communicator the values are left as they are. Syncs. */
 nau_status nau_allreduce(nau_ctx* ctx, double* values, int count, int op);
 /* Ranks of the context's communicator (1 without nau_comm_init). */
 int nau_comm_size(nau_ctx* ctx);
-/* The primitive under both: swap device row blocks (width doubles per row) with
- * the left / right neighbours; received blocks stay valid until the next call. */
-nau_status nau_comm_swap(nau_ctx* ctx, const double* to_left, long n_left, const double* to_right,
-                         long n_right, int width, const double** from_left, long* nf_left,
-                         const double** from_right, long* nf_right);
 
 /* ---- result frames and hot start (frames.cu) ----
  * Legacy VTK PolyData exactly as the reference writes it (io/vtk.cpp:193-304):

@@ -78,6 +78,7 @@ void free_particles(nau_ctx* c) {
     dfree(c->d_p4);
     dfree(c->d_skey);
     dfree(c->d_skey_s);
+    dfree(c->d_upd);
     c->cap = 0;
 }
 
@@ -104,6 +105,7 @@ nau_status alloc_particle_arrays(nau_ctx* c, long cap) {
     NAU_CUDA(dalloc(&c->d_p4, cap));
     NAU_CUDA(dalloc(&c->d_skey, cap));
     NAU_CUDA(dalloc(&c->d_skey_s, cap));
+    NAU_CUDA(dalloc(&c->d_upd, cap));
     return NAU_OK;
 }
 
@@ -248,6 +250,7 @@ Geo make_geo(nau_ctx* c) {
     g.cell_count = c->d_cell_count;
     g.nact = c->d_cell_start + c->dom.ncells;
     g.p4 = c->d_p4;
+    g.upd = c->ghost_field >= 0 ? c->d_upd : nullptr;
     return g;
 }
 
@@ -927,11 +930,29 @@ nau_status nau_symplectic_step(nau_ctx* c, int v, int vdot, int mask, double dt)
     return NAU_OK;
 }
 
-nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
+// The deck's three passes (nau_wcsph_pass); nau_wcsph_step runs them in order.
+nau_status nau_wcsph_pass(nau_ctx* c, const nau_wcsph_params* p, int pass) {
     int ids[5] = {p->f_rho, p->f_p, p->f_v, p->f_vdot, p->f_mask};
     for (int k = 0; k < 5; ++k)
         if (!(k == 4 && ids[k] < 0) && !field_ok(c, ids[k])) return fail(c, NAU_ERR_ARG, "bad field id");
     if (!(p->radius > 0.0)) return fail(c, NAU_ERR_RUNTIME, "influence radius must be positive");
+    if (pass < 0 || pass > 2) return fail(c, NAU_ERR_ARG, "nau_wcsph_pass: pass is 0, 1 or 2");
+    if (pass == 2) {  // v = euler(v, vdot*mask, dt); r = euler(r, v, dt); boundary shift
+        nau::launch_symplectic(c, c->fields[p->f_v].d, c->fields[p->f_vdot].d,
+                               p->f_mask >= 0 ? c->fields[p->f_mask].d : nullptr, p->dt);
+        c->dirty = true;
+        c->wcsph_rev = -1;
+        return NAU_OK;
+    }
+    if (pass == 1) {  // the momentum pass reads what the density pass of this build wrote
+        if (c->wcsph_rev != c->rebuild_count || c->dirty)
+            return fail(c, NAU_ERR_ARG, "nau_wcsph_pass: the momentum pass needs the density pass first");
+        if (c->mode == NAU_MODE_FAST)
+            nau::launch_wcsph_fast(c, p, c->d_aux, c->wcsph_lists, 2);
+        else
+            nau::launch_wcsph(c, p, c->wcsph_lists != 0, 2);
+        return NAU_OK;
+    }
     if (c->dirty || !c->built_once) {
         // rho, p (density pass) and vdot (momentum pass) are written for every active
         // particle before anything reads them: the build moves their inactive slots only
@@ -952,14 +973,20 @@ nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
         c->last_wcsph_path = (c->mode == NAU_MODE_FAST ? NAU_PATH_FAST : 0) | (lists << 2) |
                              (img ? NAU_PATH_IMAGES : 0);
     }
-    if (c->mode == NAU_MODE_FAST) {
-        nau::launch_wcsph_fast(c, p, c->d_aux, lists);
-        nau::launch_symplectic(c, c->fields[p->f_v].d, c->fields[p->f_vdot].d,
-                               p->f_mask >= 0 ? c->fields[p->f_mask].d : nullptr, p->dt);
-    } else {
-        nau::launch_wcsph(c, p, lists != 0);
+    if (c->mode == NAU_MODE_FAST)
+        nau::launch_wcsph_fast(c, p, c->d_aux, lists, 1);
+    else
+        nau::launch_wcsph(c, p, lists != 0, 1);
+    c->wcsph_lists = lists;
+    c->wcsph_rev = c->rebuild_count;
+    return NAU_OK;
+}
+
+nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
+    for (int pass = 0; pass < 3; ++pass) {
+        nau_status s = nau_wcsph_pass(c, p, pass);
+        if (s != NAU_OK) return s;
     }
-    c->dirty = true;
     return NAU_OK;
 }
 

@@ -280,7 +280,7 @@ __global__ void k_reorder(DomainDev d, long n, const int* perm, const int* orig,
                           const uint8_t* active, int* orig_s, int* key_s, uint8_t* active_s,
                           float4* xl, double4* p4, const int* skey, int* skey_s,
                           ReorderTable t, HalfOut ho, const int* cell_start,
-                          const int* cell_count) {
+                          const int* cell_count, const double* ghost, uint8_t* upd) {
     long s = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (s >= n) return;
     int k = perm[s];
@@ -310,6 +310,7 @@ __global__ void k_reorder(DomainDev d, long n, const int* perm, const int* orig,
         xl[s] = p;
     }
     p4[s] = make_double4(x[0], x[1], x[2], 0.0);
+    if (ghost) upd[s] = ghost[k] == 0.0;
     if (ho.h && act) write_half<DIM>(d, ho, s, kk, x, cell_start, cell_count);
 }
 
@@ -338,6 +339,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_nlist(const __grid_constant__
                                                          int* over, const __grid_constant__ HalfGrid hg) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= *g.nact) return;
+    if (is_ghost(g, k)) {  // a ghost is never evaluated: no list
+        count[k] = 0;
+        return;
+    }
     uint2* lst = reinterpret_cast<uint2*>(list) + nlist_base(k, cap);
     const float pre_r = (float)radius;
     int cnt = 0, nrec = 0;
@@ -364,6 +369,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_nlist_pair(const __grid_const
     const int nact = *g.nact;
     const int k0 = 2 * t;
     if (k0 >= nact) return;
+    if (is_ghost(g, k0) && (k0 + 1 >= nact || is_ghost(g, k0 + 1))) {  // ghosts only: no list
+        count[t] = 0;
+        return;
+    }
     uint4* lst = reinterpret_cast<uint4*>(list) + (size_t)(t >> 5) * cap * 32 + (t & 31);
     int cnt = 0, nrec = 0;
     build_pair_list<DIM>(g, xl, hg, radius, k0, k0 + 1 < nact,
@@ -505,7 +514,10 @@ void launch_build_cells(nau_ctx* c) {
                                                       c->d_active, c->d_orig_s, c->d_key_s,
                                                       c->d_active_s, want_xl ? c->d_xl : nullptr,
                                                       c->d_p4, c->d_skey, c->d_skey_s, t, ho,
-                                                      c->d_cell_start, c->d_cell_count);
+                                                      c->d_cell_start, c->d_cell_count,
+                                                      c->ghost_field >= 0 ? c->fields[c->ghost_field].d
+                                                                          : nullptr,
+                                                      c->d_upd);
     };
     if (c->dom.dim == 3) reorder(k_reorder<3>);
     else if (c->dom.dim == 2) reorder(k_reorder<2>);

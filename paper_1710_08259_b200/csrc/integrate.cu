@@ -50,9 +50,9 @@ __global__ void k_euler(long n, int comps, const uint8_t* active, const int* ori
 // One thread per particle: the two euler equations then the boundary shift of r.
 __global__ void k_symplectic(DomainDev d, long n, double* pos, double* v, const double* vdot,
                              const double* mask, double dt, uint8_t* active, const int* orig,
-                             DevErr* err) {
+                             DevErr* err, const uint8_t* upd) {
     long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (k >= n || !active[k]) return;
+    if (k >= n || !active[k] || (upd && !upd[k])) return;  // ghosts: owned elsewhere
     const double mk = mask ? mask[k] : 1.0;
     double vn[3];
     bool bad = false;
@@ -114,7 +114,7 @@ template <int DIM, int KF, bool LIST>
 __global__ void __launch_bounds__(kThreads) k_wcsph_density(const __grid_constant__ WcsphArgs a) {
     const Geo& g = a.g;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = k < *g.nact;
+    const bool valid = k < *g.nact && !is_ghost(g, k);
     const int kk = valid ? k : 0;
     const long n = g.n;
     double xi[3] = {0.0, 0.0, 0.0};
@@ -152,7 +152,7 @@ template <int DIM, int KF, bool LIST>
 __global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_constant__ WcsphArgs a) {
     const Geo& g = a.g;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    bool valid = k < *g.nact;
+    bool valid = k < *g.nact && !is_ghost(g, k);
     const int kk = valid ? k : 0;
     const long n = g.n;
     double xi[3] = {0.0, 0.0, 0.0}, v_i[3] = {0.0, 0.0, 0.0};
@@ -261,31 +261,36 @@ __global__ void k_reduce_partial(long n, int comps, int kind, const uint8_t* act
 }
 
 template <int DIM, bool LIST>
-void wcsph_launch(nau_ctx* c, const WcsphArgs& a, int kf) {
+void wcsph_launch(nau_ctx* c, const WcsphArgs& a, int kf, int passes) {
     const int blocks = (int)((c->n + kThreads - 1) / kThreads);
-    prof_begin(c, 200);
-    if (kf == NAU_K_CUBIC) {
-        k_wcsph_density<DIM, NAU_K_CUBIC, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
-    } else {
-        k_wcsph_density<DIM, NAU_K_WENDLAND, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
+    if (passes & 1) {
+        prof_begin(c, 200);
+        if (kf == NAU_K_CUBIC) {
+            k_wcsph_density<DIM, NAU_K_CUBIC, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
+        } else {
+            k_wcsph_density<DIM, NAU_K_WENDLAND, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
+        }
+        prof_end(c, 200);
+        c->launches++;
     }
-    prof_end(c, 200);
-    prof_begin(c, 201);
-    if (kf == NAU_K_CUBIC) {
-        k_wcsph_momentum<DIM, NAU_K_CUBIC, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
-    } else {
-        k_wcsph_momentum<DIM, NAU_K_WENDLAND, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
+    if (passes & 2) {
+        prof_begin(c, 201);
+        if (kf == NAU_K_CUBIC) {
+            k_wcsph_momentum<DIM, NAU_K_CUBIC, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
+        } else {
+            k_wcsph_momentum<DIM, NAU_K_WENDLAND, LIST><<<blocks, kThreads, 0, c->stream>>>(a);
+        }
+        prof_end(c, 201);
+        c->launches++;
     }
-    prof_end(c, 201);
-    c->launches += 2;
 }
 
 template <int DIM>
-void wcsph_launch_dim(nau_ctx* c, const WcsphArgs& a, int kf) {
+void wcsph_launch_dim(nau_ctx* c, const WcsphArgs& a, int kf, int passes) {
     if (a.nl.e)
-        wcsph_launch<DIM, true>(c, a, kf);
+        wcsph_launch<DIM, true>(c, a, kf, passes);
     else
-        wcsph_launch<DIM, false>(c, a, kf);
+        wcsph_launch<DIM, false>(c, a, kf, passes);
 }
 
 }  // namespace
@@ -309,12 +314,13 @@ void launch_symplectic(nau_ctx* c, double* v, const double* vdot, const double* 
     prof_begin(c, 301);
     k_symplectic<<<blocks_for(c->n), kBlock, 0, c->stream>>>(c->dom, c->n, c->fields[0].d, v, vdot,
                                                               mask, dt, c->d_active, c->d_orig,
-                                                              c->d_err);
+                                                              c->d_err,
+                                                              c->ghost_field >= 0 ? c->d_upd : nullptr);
     prof_end(c, 301);
     c->launches++;
 }
 
-void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p, bool lists) {
+void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p, bool lists, int passes) {
     if (c->n == 0) return;
     WcsphArgs a;
     a.nl = NList{lists ? c->d_nlist : nullptr, c->d_ncount, c->nl_cap};
@@ -336,12 +342,10 @@ void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p, bool lists) {
     a.vdot = c->fields[p->f_vdot].d;
     a.err = c->d_err;
     switch (c->dom.dim) {
-        case 1: wcsph_launch_dim<1>(c, a, p->kernel_family); break;
-        case 2: wcsph_launch_dim<2>(c, a, p->kernel_family); break;
-        default: wcsph_launch_dim<3>(c, a, p->kernel_family); break;
+        case 1: wcsph_launch_dim<1>(c, a, p->kernel_family, passes); break;
+        case 2: wcsph_launch_dim<2>(c, a, p->kernel_family, passes); break;
+        default: wcsph_launch_dim<3>(c, a, p->kernel_family, passes); break;
     }
-    const double* mask = p->f_mask >= 0 ? c->fields[p->f_mask].d : nullptr;
-    launch_symplectic(c, c->fields[p->f_v].d, c->fields[p->f_vdot].d, mask, p->dt);
 }
 
 void launch_reduce(nau_ctx* c, int kind, const double* f, int comps, double* h_out) {

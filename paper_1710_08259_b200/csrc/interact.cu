@@ -189,7 +189,7 @@ template <int DIM, int OP>
 __global__ void __launch_bounds__(kThreads, NAU_DEM_MINB) k_dem(const __grid_constant__ DemArgs a) {
     const Geo& g = a.g;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = k < *g.nact;
+    const bool valid = k < *g.nact && !is_ghost(g, k);
     const int kk = valid ? k : 0;
     const long n = g.n;
     constexpr bool kImagesOnly = OP == NAU_OP_DEM_BOUNDARY;

@@ -87,7 +87,12 @@ struct Geo {
     const int* cell_start;
     const int* cell_count;
     const int* nact;  // == cell_start[ncells]
+    const uint8_t* upd;  // per slot: 0 = ghost (a neighbour only, never updated); null: all
 };
+
+// Ghost test of a slot (slab runs, nau_set_ghost_field): ghosts take part in the sums
+// as neighbours but are not evaluated or integrated.
+__device__ __forceinline__ bool is_ghost(const Geo& g, long k) { return g.upd && !g.upd[k]; }
 
 struct FieldBuf {
     int rows = 0, cols = 0;
@@ -381,6 +386,8 @@ struct nau_ctx {
     long xl_rev = -1;         // rebuild_count d_xl belongs to (ensure_xl)
     bool xl_used = true;      // a sweep read d_xl since the last build: k_reorder writes it
     unsigned long long reorder_skip = 0;  // fields the next build moves for inactive slots only
+    int ghost_field = -1;     // nau_set_ghost_field: scalar field, != 0 marks a ghost
+    uint8_t* d_upd = nullptr; // per slot (written by the reorder): 1 = updated, 0 = ghost
     // asynchronous host I/O (nau_upload_async / nau_download_async): one copy
     // stream per direction, per-field double-buffered staging in original order
     struct IoStage {
@@ -399,6 +406,8 @@ struct nau_ctx {
     std::vector<IoStage> io_up, io_down;  // indexed by field id
     int mode = NAU_MODE_EXACT;
     int last_wcsph_path = -1;  // nau_wcsph_path: which kernels the last nau_wcsph_step ran
+    int wcsph_lists = -1;      // neighbour source of the density pass, reused by the momentum pass
+    long wcsph_rev = -1;       // ... for this cell build
     int* d_cell_start = nullptr;  // ncells + 2
     int* d_cell_count = nullptr;  // ncells + 1
     int* d_cursor = nullptr;      // ncells + 1
@@ -457,7 +466,8 @@ void launch_commit_if_ok(nau_ctx* c, const double* src, double* dst);
 void launch_euler(nau_ctx* c, const double* x, const double* xdot, double dt, double* out,
                   int comps);
 void launch_symplectic(nau_ctx* c, double* v, const double* vdot, const double* mask, double dt);
-void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p, bool lists);
+// passes: 1 density/EOS, 2 momentum (the symplectic update is launch_symplectic)
+void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p, bool lists, int passes);
 void launch_reduce(nau_ctx* c, int kind, const double* f, int comps, double* h_out);
 // fast.cu
 bool fast_supports(int op, int a_rows, int a_cols, int dim);
@@ -465,5 +475,5 @@ void launch_g11_l0_fast(nau_ctx* c, int kf, int kdim, const Opd* ops, double* ou
                         double* out_l, bool lists);
 void launch_interact_fast(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, double* out,
                           int a_rows, bool lists = false);
-void launch_wcsph_fast(nau_ctx* c, const nau_wcsph_params* p, double4* vp, int lists);
+void launch_wcsph_fast(nau_ctx* c, const nau_wcsph_params* p, double4* vp, int lists, int passes);
 }  // namespace nau

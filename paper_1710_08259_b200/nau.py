@@ -48,7 +48,10 @@ EXPORTS = [
     "nau_allreduce", "nau_comm_size", "nau_field_shape", "nau_case_create", "nau_case_destroy",
     "nau_case_constant", "nau_case_variable", "nau_case_set_variable", "nau_case_get_variable",
     "nau_case_field", "nau_case_equation", "nau_case_equation_count", "nau_case_solve_equation",
-    "nau_case_solve_step", "nau_case_last_error",
+    "nau_case_solve_step", "nau_case_last_error", "nau_wcsph_pass", "nau_select_x", "nau_reserve",
+    "nau_rebuild_rows", "nau_histogram_x", "nau_set_ghost_field", "nau_wcsph_pack_rho_p",
+    "nau_wcsph_ghost_update", "nau_slab_bounds", "nau_slab_rebalance", "nau_pack_fields",
+    "nau_unpack_fields", "nau_wcsph_ghost_payload",
 ]
 
 
@@ -170,9 +173,14 @@ def load():
         "nau_comm_unique_id": (i, [vp]),
         "nau_comm_init": (i, [vp, vp, i, i]),
         "nau_comm_destroy": (None, [vp]),
-        "nau_slab_config": (i, [vp, i, vp, i, i, i, i]),
+        "nau_slab_config": (i, [vp, i, vp, i, d, i, i]),
+        "nau_slab_bounds": (i, [vp, vp]),
+        "nau_slab_rebalance": (i, [vp, i]),
         "nau_migrate": (i, [vp]),
-        "nau_halo_exchange": (i, [vp]),
+        "nau_halo_exchange": (i, [vp, vp, i]),
+        "nau_pack_fields": (i, [vp, vp, l, vp, i, vp]),
+        "nau_unpack_fields": (i, [vp, vp, l, vp, i, vp]),
+        "nau_wcsph_ghost_payload": (i, [vp, C.POINTER(WcsphParams)]),
         "nau_comm_swap": (i, [vp, vp, l, vp, l, i, vp, vp, vp, vp]),
         "nau_write_vtk": (i, [vp, C.c_char_p, i, vp]),
         "nau_vtk_read": (i, [C.c_char_p, vp]),
@@ -198,6 +206,14 @@ def load():
         "nau_case_solve_equation": (i, [vp, i]),
         "nau_case_solve_step": (i, [vp]),
         "nau_case_last_error": (C.c_char_p, [vp, C.POINTER(l)]),
+        "nau_wcsph_pass": (i, [vp, C.POINTER(WcsphParams), i]),
+        "nau_select_x": (i, [vp, i, d, d, i, d, d, vp, C.POINTER(l)]),
+        "nau_reserve": (i, [vp, l]),
+        "nau_rebuild_rows": (i, [vp, vp, l, vp, l, i]),
+        "nau_histogram_x": (i, [vp, i, d, d, i, i, d, d, vp]),
+        "nau_set_ghost_field": (i, [vp, i]),
+        "nau_wcsph_pack_rho_p": (i, [vp, C.POINTER(WcsphParams), vp, l, vp]),
+        "nau_wcsph_ghost_update": (i, [vp, C.POINTER(WcsphParams), vp, l, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -320,17 +336,28 @@ class Context:
         buf = (C.c_ubyte * 128).from_buffer_copy(uid)
         self._check(self.L.nau_comm_init(self.h, buf, nranks, rank))
 
-    def slab_config(self, axis, bounds, periodic, ghost_planes=2, gid="gid", ghost="ghost"):
-        b = np.ascontiguousarray(bounds, dtype=np.int32)
+    def slab_config(self, axis, bounds, periodic, radius, gid="gid", flag="ghost"):
+        """x-threshold slabs: bounds = nranks + 1 coordinates (nau_slab_config)."""
+        b = np.ascontiguousarray(bounds, dtype=np.float64)
+        self._slab_nb = len(b)
         self._check(self.L.nau_slab_config(self.h, axis, b.ctypes.data, int(periodic),
-                                           ghost_planes, self._fid(gid), self._fid(ghost)))
+                                           float(radius), self._fid(gid), self._fid(flag)))
+
+    def slab_bounds(self):
+        out = np.zeros(self._slab_nb)
+        self._check(self.L.nau_slab_bounds(self.h, out.ctypes.data))
+        return out.tolist()
 
     def migrate(self):
         self._check(self.L.nau_migrate(self.h))
         self.n = self.L.nau_particle_count(self.h)
 
-    def halo_exchange(self):
-        self._check(self.L.nau_halo_exchange(self.h))
+    def halo_exchange(self, fields):
+        ids = np.ascontiguousarray([self._fid(f) for f in fields], dtype=np.int32)
+        self._check(self.L.nau_halo_exchange(self.h, ids.ctypes.data, len(ids)))
+
+    def slab_rebalance(self, nbins=4096):
+        self._check(self.L.nau_slab_rebalance(self.h, nbins))
         self.n = self.L.nau_particle_count(self.h)
 
     def comm_swap(self, to_left, to_right):
@@ -605,6 +632,10 @@ class Context:
 
     def wcsph_step(self, p: WcsphParams):
         self._check(self.L.nau_wcsph_step(self.h, C.byref(p)))
+
+    def wcsph_pass(self, p: WcsphParams, k: int):
+        """0 cells + list + density/EOS, 1 momentum, 2 symplectic update (nau_wcsph_pass)."""
+        self._check(self.L.nau_wcsph_pass(self.h, C.byref(p), k))
 
     def dem_step(self, p: DemParams):
         self._check(self.L.nau_dem_step(self.h, C.byref(p)))

@@ -22,8 +22,8 @@ def make_system(scene):
     return ps, st
 
 
-def step(ps, st, prm, kfamily=port.K_WENDLAND):
-    """One solve_step of the deck; mutates ps (positions/active/cells) and st."""
+def density(ps, st, prm, kfamily=port.K_WENDLAND):
+    """rho = sph_S(one, mass, one, K, R); p = B*((rho/rho0)^gam - 1)."""
     dim = ps.dom.dim
     act = ps.active.astype(bool)
     R, m = prm["radius"], prm["mass"]
@@ -38,17 +38,42 @@ def step(ps, st, prm, kfamily=port.K_WENDLAND):
     powed = np.array([math.pow(x, prm["gamma"]) for x in ratio.tolist()], dtype=np.float64)
     p[0, act] = prm["B"] * (powed - 1.0)
     st["p"] = p
-    G = ps.interact(port.SPH_G11, [p, m, rho, R], (dim, 1), kfamily=kfamily, kdim=dim)
+    return st
+
+
+def momentum(ps, st, prm, kfamily=port.K_WENDLAND):
+    """vdot = -1/rho*sph_G11(p, mass, rho, K, R) + visc*sph_A(v, mass, rho, K, R) + g."""
+    dim = ps.dom.dim
+    act = ps.active.astype(bool)
+    R, m = prm["radius"], prm["mass"]
+    rho = st["rho"]
+    G = ps.interact(port.SPH_G11, [st["p"], m, rho, R], (dim, 1), kfamily=kfamily, kdim=dim)
     A = ps.interact(port.SPH_A, [st["v"], m, rho, R], (dim, 1), kfamily=kfamily, kdim=dim)
     g = np.asarray(prm["g"], dtype=np.float64).reshape(dim, 1)
     vdot = st["vdot"].copy()
     vdot[:, act] = ((-1.0 / rho[:, act]) * G[:, act] + prm["visc"] * A[:, act]) + g
     st["vdot"] = vdot
+    return st
+
+
+def integrate(ps, st, prm, upd=None):
+    """v = euler(v, vdot*mask, dt); r = euler(r, v, dt); boundary shift. upd: the particles
+    updated (slab ghosts are not)."""
+    act = ps.active.astype(bool)
+    if upd is not None:
+        act = act & upd
     v = st["v"].copy()
-    v[:, act] = v[:, act] + prm["dt"] * (st["mask"][:, act] * vdot[:, act])
+    v[:, act] = v[:, act] + prm["dt"] * (st["mask"][:, act] * st["vdot"][:, act])
     st["v"] = v
     pos = ps.pos
     pos[:, act] = pos[:, act] + prm["dt"] * v[:, act]
     ps.boundary_shift()  # case.cpp:59-62, then dirty
     ps.tables = None
     return st
+
+
+def step(ps, st, prm, kfamily=port.K_WENDLAND):
+    """One solve_step of the deck; mutates ps (positions/active/cells) and st."""
+    density(ps, st, prm, kfamily)
+    momentum(ps, st, prm, kfamily)
+    return integrate(ps, st, prm)

@@ -895,17 +895,16 @@ def test_slab_ranks_with_rebalancing_match_plain(ctx, world):
             sl.sc = scene()
             sl.setup(c)
             sc = sl.sc
-            ncx = sc.max_cells[0] - sc.min_cells[0]
-            # skewed start (two-plane slabs, one huge): re-balancing must move bounds
-            # past whole slabs, so particles hop over a rank
-            skew = [2 * i for i in range(world)] + [ncx]
+            R = sc.params["radius"]
+            lo, hi = sc.min_cells[0] * sc.cell_size[0], sc.max_cells[0] * sc.cell_size[0]
+            # skewed start (2R-wide slabs, one huge): re-balancing must move bounds past
+            # whole slabs, so particles hop over a rank
+            skew = [lo + 2 * R * i for i in range(world)] + [hi]
             import torch
-            rows = slab_mod.initial_rows(sc, sl.FIELDS, skew, rank, ncx, False)
+            rows = slab_mod.initial_rows(sc, sl.FIELDS, skew, rank, R, False)
             sl.backend.load(torch.from_numpy(rows).to(sl.backend.device))
             ex = _ThreadExchanger(hub, rank, False, sl.backend.device)
-            r = slab_mod.SlabRank(sl.backend, ex, skew, ncx, False, rebalance_every=3,
-                                  x_lo=sc.min_cells[0] * sc.cell_size[0],
-                                  cell_size=sc.cell_size[0])
+            r = slab_mod.SlabRank(sl.backend, ex, skew, R, False, rebalance_every=3, nbins=256)
             drv[rank] = r
             for _ in range(steps):
                 r.step()
@@ -978,15 +977,16 @@ def test_native_comm_swap_on_a_one_rank_ring():
         c.add_field("gid", 1, 1, np.arange(4.0))
         c.add_field("ghost", 1, 1, 0.0)
         c.comm_init(nau.Context.comm_unique_id(), 1, 0)
-        c.slab_config(0, [0, 4], True, 1)
+        c.slab_config(0, [0.0, 1.0], True, 0.25)
+        assert c.slab_bounds() == [0.0, 1.0]
         a = torch.arange(21, dtype=torch.float64, device="cuda").reshape(7, 3)
         b = -torch.arange(6, dtype=torch.float64, device="cuda").reshape(2, 3)
         fl, fr = c.comm_swap(a, b)
         assert torch.equal(fr, a) and torch.equal(fl, b)
         fl, fr = c.comm_swap(b[:0], a)
         assert fr.shape == (0, 3) and torch.equal(fl, a)
-        with pytest.raises(nau.NauError):  # bounds must cover the axis
-            c.slab_config(0, [0, 3], True, 1)
+        with pytest.raises(nau.NauError):  # bounds must rise
+            c.slab_config(0, [1.0, 0.0], True, 0.25)
     finally:
         c.close()
 
