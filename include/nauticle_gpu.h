@@ -217,6 +217,10 @@ nau_status nau_wcsph_step(nau_ctx* ctx, const nau_wcsph_params* prm);
  * them): 0 = cell build + neighbour list + density/EOS, 1 = momentum
  * (after pass 0 of the same build), 2 = symplectic update + boundary shift. */
 nau_status nau_wcsph_pass(nau_ctx* ctx, const nau_wcsph_params* prm, int pass);
+/* nau_wcsph_step runs without host synchronisation and, after two warm-up calls, is
+ * captured into a CUDA graph replayed for later steps that start from the same host
+ * state (default on; NAU_GRAPHS=0 in the environment or on = 0 here disables it). */
+nau_status nau_set_graphs(nau_ctx* ctx, int on);
 
 /* DEM deck (BASELINE cfg3), the reference's equation form:
  *   vdot = law(v, R, P, Q, m, cf, Rs) + g;  v = euler(v, vdot, dt);  r = euler(r, v, dt)

@@ -3,6 +3,7 @@
 // operator registry (kOps[], src/interactions.cpp:259-269).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -85,6 +86,8 @@ void free_particles(nau_ctx* c) {
 nau_status ensure_field_storage(nau_ctx* c, FieldBuf& f);
 
 }  // namespace
+
+extern "C" void nau_release_graphs(nau_ctx* c);  // the wcsph step graphs (below)
 
 namespace nau {
 
@@ -344,6 +347,7 @@ void nau_destroy(nau_ctx* c) {
         cudaStreamSynchronize(c->s_d2h);
     }
     if (c->stream) cudaStreamSynchronize(c->stream);
+    nau_release_graphs(c);
     nau_comm_destroy(c);
     io_release(c);
     free_particles(c);
@@ -354,6 +358,8 @@ void nau_destroy(nau_ctx* c) {
     dfree(c->d_nlist);
     dfree(c->d_ncount);
     dfree(c->d_nover);
+    dfree(c->d_work);
+    dfree(c->d_nwork);
     if (c->h_nover) cudaFreeHost(c->h_nover);
     c->h_nover = c->h_nover_dev = nullptr;
     dfree(c->d_hq);
@@ -966,7 +972,8 @@ nau_status nau_wcsph_pass(nau_ctx* c, const nau_wcsph_params* p, int pass) {
     for (int a = 1; a < c->dom.dim; ++a) min_cs = std::min(min_cs, c->dom.cs[a]);
     const bool pairs = c->mode == NAU_MODE_FAST && p->kernel_family == NAU_K_WENDLAND &&
                        p->radius <= min_cs;
-    const int lists = nau::nlist_for(c, p->radius, c->mode == NAU_MODE_EXACT, pairs);
+    // no host synchronisation: an overflowing list is swept by the fallback pass
+    const int lists = nau::nlist_for(c, p->radius, c->mode == NAU_MODE_EXACT, pairs, true);
     {
         int img = 0;
         for (int a = 0; a < c->dom.dim; ++a) img |= c->dom.kind[a] != NAU_CUTOFF;
@@ -982,11 +989,186 @@ nau_status nau_wcsph_pass(nau_ctx* c, const nau_wcsph_params* p, int pass) {
     return NAU_OK;
 }
 
-nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
+// ---- CUDA graphs of the WCSPH step ----
+// One nau_wcsph_step is ~15 launches and memsets with no host synchronisation (async
+// neighbour lists). After two warm-up calls a step is captured into a graph together
+// with the host state it started from (every buffer pointer the launches use, the
+// pointer swaps of the cell build, cache keys relative to the rebuild counter, flags,
+// the parameters) and the state it left. A later call that starts from the same state
+// replays the graph and applies the recorded successor state on the host. Steps
+// alternate between two buffer parities, so two graphs cover a run. Profiling, a
+// capacity change or any mismatch runs the plain path (and may capture anew).
+struct HostState {
+    std::vector<uintptr_t> ptr;  // buffers / sizes that must match for a replay
+    long n = 0, nl_rel = 0, hq_rel = 0, xl_rel = 0, wcsph_rel = 0;
+    bool dirty = false, built_once = false, xl_used = false, hq_used = false, nl_async = false;
+    unsigned long long reorder_skip = 0;
+    double nl_radius = 0.0;
+    bool nl_ordered = false, nl_pairs = false;
+    int nl_cap = 0, wcsph_lists = 0, last_path = 0, mode = 0, ghost_field = -1;
+    nau_wcsph_params prm{};
+    std::vector<double*> fd, fa;  // field storage after the step (swapped by the build)
+    int* orig = nullptr; int* orig_s = nullptr; int* skey = nullptr; int* skey_s = nullptr;
+    int* key = nullptr; int* key_s = nullptr; uint8_t* act = nullptr; uint8_t* act_s = nullptr;
+};
+
+struct nau_ctx::StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    HostState before, after;
+    long d_rebuild = 0, kernels = 0;
+};
+
+static HostState capture_state(nau_ctx* c, const nau_wcsph_params* p) {
+    HostState h;
+    auto add = [&](const void* q) { h.ptr.push_back(reinterpret_cast<uintptr_t>(q)); };
+    add(c->d_orig); add(c->d_orig_s); add(c->d_skey); add(c->d_skey_s); add(c->d_key);
+    add(c->d_key_s); add(c->d_active); add(c->d_active_s); add(c->d_nlist); add(c->d_hq);
+    add(c->d_pstart); add(c->d_work); add(c->d_xl); add(c->d_p4); add(c->d_aux); add(c->d_upd);
+    add(reinterpret_cast<void*>(c->nl_len)); add(reinterpret_cast<void*>(c->hq_len));
+    add(reinterpret_cast<void*>(c->pstart_len)); add(reinterpret_cast<void*>(c->cap));
+    add(c->d_cell_start); add(c->d_cell_count); add(c->d_cursor); add(c->d_scan_tmp);
+    add(c->d_perm); add(c->d_perm_tmp); add(c->d_okey); add(c->d_hesc); add(c->d_nover);
+    add(c->d_ncount); add(c->d_nwork); add(c->d_pcount); add(c->d_err); add(c->h_nover_dev);
+    add(reinterpret_cast<void*>((uintptr_t)c->dom.ncells));
+    add(reinterpret_cast<void*>((uintptr_t)(c->use_nlist * 2 + c->use_pairs)));
+    add(reinterpret_cast<void*>((uintptr_t)c->dom.dim));
+    for (int a = 0; a < 3; ++a) {
+        uint64_t bits;
+        std::memcpy(&bits, &c->dom.cs[a], 8);
+        add(reinterpret_cast<void*>(bits));
+        std::memcpy(&bits, &c->dom.lo[a], 8);
+        add(reinterpret_cast<void*>(bits));
+        add(reinterpret_cast<void*>((uintptr_t)(c->dom.cells[a] * 4 + c->dom.kind[a])));
+    }
+    for (auto& f : c->fields) {
+        add(f.d); add(f.alt); add(reinterpret_cast<void*>((uintptr_t)f.live));
+        h.fd.push_back(f.d);
+        h.fa.push_back(f.alt);
+    }
+    h.n = c->n;
+    h.nl_rel = c->nl_rev - c->rebuild_count;
+    h.hq_rel = c->hq_rev - c->rebuild_count;
+    h.xl_rel = c->xl_rev - c->rebuild_count;
+    h.wcsph_rel = c->wcsph_rev - c->rebuild_count;
+    h.dirty = c->dirty; h.built_once = c->built_once; h.xl_used = c->xl_used;
+    h.hq_used = c->hq_used; h.nl_async = c->nl_async; h.reorder_skip = c->reorder_skip;
+    h.nl_radius = c->nl_radius; h.nl_ordered = c->nl_ordered; h.nl_pairs = c->nl_pairs;
+    h.nl_cap = c->nl_cap; h.wcsph_lists = c->wcsph_lists; h.last_path = c->last_wcsph_path;
+    h.mode = c->mode; h.ghost_field = c->ghost_field;
+    h.prm = *p;
+    h.orig = c->d_orig; h.orig_s = c->d_orig_s; h.skey = c->d_skey; h.skey_s = c->d_skey_s;
+    h.key = c->d_key; h.key_s = c->d_key_s; h.act = c->d_active; h.act_s = c->d_active_s;
+    return h;
+}
+
+static bool same_state(const HostState& a, const HostState& b) {
+    return a.ptr == b.ptr && a.n == b.n && a.nl_rel == b.nl_rel && a.hq_rel == b.hq_rel &&
+           a.xl_rel == b.xl_rel && a.wcsph_rel == b.wcsph_rel && a.dirty == b.dirty &&
+           a.built_once == b.built_once && a.xl_used == b.xl_used && a.hq_used == b.hq_used &&
+           a.nl_async == b.nl_async && a.reorder_skip == b.reorder_skip &&
+           a.nl_radius == b.nl_radius && a.nl_ordered == b.nl_ordered &&
+           a.nl_pairs == b.nl_pairs && a.nl_cap == b.nl_cap && a.wcsph_lists == b.wcsph_lists &&
+           a.last_path == b.last_path && a.mode == b.mode && a.ghost_field == b.ghost_field &&
+           std::memcmp(&a.prm, &b.prm, sizeof(a.prm)) == 0;
+}
+
+// The host side of a step: pointers and flags as `h`, counters advanced by d_rebuild.
+static void apply_state(nau_ctx* c, const HostState& h, long d_rebuild) {
+    c->rebuild_count += d_rebuild;
+    for (size_t f = 0; f < c->fields.size() && f < h.fd.size(); ++f) {
+        c->fields[f].d = h.fd[f];
+        c->fields[f].alt = h.fa[f];
+    }
+    c->d_orig = h.orig; c->d_orig_s = h.orig_s; c->d_skey = h.skey; c->d_skey_s = h.skey_s;
+    c->d_key = h.key; c->d_key_s = h.key_s; c->d_active = h.act; c->d_active_s = h.act_s;
+    c->nl_rev = c->rebuild_count + h.nl_rel;
+    c->hq_rev = c->rebuild_count + h.hq_rel;
+    c->xl_rev = c->rebuild_count + h.xl_rel;
+    c->wcsph_rev = c->rebuild_count + h.wcsph_rel;
+    c->dirty = h.dirty; c->built_once = h.built_once; c->xl_used = h.xl_used;
+    c->hq_used = h.hq_used; c->nl_async = h.nl_async; c->reorder_skip = h.reorder_skip;
+    c->nl_radius = h.nl_radius; c->nl_ordered = h.nl_ordered; c->nl_pairs = h.nl_pairs;
+    c->nl_cap = h.nl_cap; c->wcsph_lists = h.wcsph_lists; c->last_wcsph_path = h.last_path;
+}
+
+static void drop_graphs(nau_ctx* c) {
+    for (auto* g : c->graphs) {
+        if (g->exec) cudaGraphExecDestroy(g->exec);
+        delete g;
+    }
+    c->graphs.clear();
+    c->graph_warm = 0;
+}
+
+void nau_release_graphs(nau_ctx* c) { drop_graphs(c); }
+
+static nau_status wcsph_step_plain(nau_ctx* c, const nau_wcsph_params* p) {
     for (int pass = 0; pass < 3; ++pass) {
         nau_status s = nau_wcsph_pass(c, p, pass);
         if (s != NAU_OK) return s;
     }
+    return NAU_OK;
+}
+
+nau_status nau_wcsph_step(nau_ctx* c, const nau_wcsph_params* p) {
+    static const bool env_off = std::getenv("NAU_GRAPHS") && std::atoi(std::getenv("NAU_GRAPHS")) == 0;
+    if (!c->use_graphs || env_off || c->profile || c->n == 0) return wcsph_step_plain(c, p);
+    // a list overflow published by an earlier step grows the capacity on the plain path
+    if (c->h_nover && *(volatile int*)c->h_nover > c->nl_cap && c->nl_cap < 1024) {
+        drop_graphs(c);
+        return wcsph_step_plain(c, p);
+    }
+    const HostState before = capture_state(c, p);
+    for (auto* g : c->graphs)
+        if (same_state(g->before, before)) {
+            if (cudaGraphLaunch(g->exec, c->stream) != cudaSuccess) {
+                cudaGetLastError();
+                drop_graphs(c);
+                c->use_graphs = false;
+                return wcsph_step_plain(c, p);
+            }
+            apply_state(c, g->after, g->d_rebuild);
+            c->launches += g->kernels;
+            return NAU_OK;
+        }
+    if (c->graph_warm < 2 || c->graphs.size() >= 4) {  // allocations settle first
+        ++c->graph_warm;
+        if (c->graphs.size() >= 4) drop_graphs(c);
+        return wcsph_step_plain(c, p);
+    }
+    const long r0 = c->rebuild_count, l0 = c->launches;
+    const std::string err0 = c->last_error;
+    cudaGraph_t graph = nullptr;
+    bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    nau_status st = ok ? wcsph_step_plain(c, p) : NAU_ERR_CUDA;
+    if (ok) ok = cudaStreamEndCapture(c->stream, &graph) == cudaSuccess && st == NAU_OK;
+    cudaGraphExec_t exec = nullptr;
+    if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {  // undo the host side of the captured step and run it for real
+        cudaGetLastError();
+        if (exec) cudaGraphExecDestroy(exec);
+        apply_state(c, before, 0);
+        c->rebuild_count = r0;
+        c->launches = l0;
+        c->last_error = err0;
+        c->use_graphs = false;
+        return wcsph_step_plain(c, p);
+    }
+    auto* g = new nau_ctx::StepGraph;
+    g->exec = exec;
+    g->before = before;
+    g->after = capture_state(c, p);
+    g->d_rebuild = c->rebuild_count - r0;
+    g->kernels = c->launches - l0;
+    c->graphs.push_back(g);
+    if (cudaGraphLaunch(exec, c->stream) != cudaSuccess) return fail(c, NAU_ERR_CUDA, "graph launch failed");
+    return NAU_OK;
+}
+
+nau_status nau_set_graphs(nau_ctx* c, int on) {
+    drop_graphs(c);
+    c->use_graphs = on != 0;
     return NAU_OK;
 }
 

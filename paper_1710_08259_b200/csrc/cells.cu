@@ -336,7 +336,8 @@ template <int DIM, bool ORDERED>
 __global__ void __launch_bounds__(kSweepThreads) k_nlist(const __grid_constant__ Geo g,
                                                          const float4* xl, double radius,
                                                          uint32_t* list, int* count, int cap,
-                                                         int* over, const __grid_constant__ HalfGrid hg) {
+                                                         int* over, const __grid_constant__ HalfGrid hg,
+                                                         int* work, int* nwork) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= *g.nact) return;
     if (is_ghost(g, k)) {  // a ghost is never evaluated: no list
@@ -354,7 +355,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_nlist(const __grid_constant__
     else
         build_list<DIM, ORDERED, true>(g, xl, k, pre_r, emit);
     count[k] = cnt;
-    if (nrec > cap) atomicMax(over, nrec);
+    if (nrec > cap) {
+        atomicMax(over, nrec);
+        if (work) {  // async build: this slot goes to the fallback pass
+            count[k] = -1;
+            work[atomicAdd(nwork, 1)] = k;
+        }
+    }
 }
 
 // Paired lists (sweep.cuh consume_pairs): thread t = slots 2t, 2t+1; count[t] =
@@ -364,7 +371,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_nlist_pair(const __grid_const
                                                               const float4* xl, double radius,
                                                               uint32_t* list, int* count, int cap,
                                                               int* over,
-                                                              const __grid_constant__ HalfGrid hg) {
+                                                              const __grid_constant__ HalfGrid hg,
+                                                              int* work, int* nwork) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int nact = *g.nact;
     const int k0 = 2 * t;
@@ -384,7 +392,16 @@ __global__ void __launch_bounds__(kSweepThreads) k_nlist_pair(const __grid_const
         }
     });
     count[t] = cnt;
-    if (nrec > cap) atomicMax(over, nrec);
+    if (nrec > cap) {
+        atomicMax(over, nrec);
+        if (work) {  // async build: both slots go to the fallback pass
+            count[t] = -1;
+            const bool has1 = k0 + 1 < nact;
+            const int w = atomicAdd(nwork, has1 ? 2 : 1);
+            work[w] = k0;
+            if (has1) work[w + 1] = k0 + 1;
+        }
+    }
 }
 
 // fp16 cell-relative coordinates (sweep.cuh HalfGrid): padded cell sizes, then one
@@ -408,21 +425,26 @@ __global__ void k_half_coords(DomainDev d, long n, const double* pos, const int*
 }
 
 // fp32 pre-filter coordinates xl[s] = (float)(x - lo) (NaN when inactive): the sweeps'
-// conservative pre-filter input. ONLY_ESCAPED: the fp16 list path's fallback, a no-op
-// unless some particle escaped its cell box.
-template <bool ONLY_ESCAPED>
+// conservative pre-filter input. Grid-strided. cond0 / cond1 (device words, may be
+// null): a no-op unless one of them is non-zero — the list builds' fallbacks (a
+// particle escaped its cell box for the fp16 pre-filter; a list overflowed, so the
+// fallback pass sweeps).
 __global__ void k_xl(DomainDev d, long n, const double* pos, const int* key, float4* xl,
-                     const int* escaped) {
-    const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (k >= n || (ONLY_ESCAPED && *escaped == 0)) return;
-    float4 p = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
-    if (key[k] < d.ncells) {
-        float v[3] = {0.f, 0.f, 0.f};
-        for (int a = 0; a < d.dim; ++a) v[a] = (float)(pos[a * n + k] - d.lo[a]);
-        p = make_float4(v[0], v[1], v[2], 0.f);
+                     const int* cond0, const int* cond1) {
+    if ((cond0 || cond1) && !((cond0 && *cond0) || (cond1 && *cond1))) return;
+    for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n;
+         k += (long)gridDim.x * blockDim.x) {
+        float4 p = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
+        if (key[k] < d.ncells) {
+            float v[3] = {0.f, 0.f, 0.f};
+            for (int a = 0; a < d.dim; ++a) v[a] = (float)(pos[a * n + k] - d.lo[a]);
+            p = make_float4(v[0], v[1], v[2], 0.f);
+        }
+        xl[k] = p;
     }
-    xl[k] = p;
 }
+
+constexpr int kXlBlocks = 148 * 8;
 
 __global__ void k_unsort(long n, int comps, const int* orig, const double* src, double* dst) {
     long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
@@ -537,8 +559,8 @@ void launch_build_cells(nau_ctx* c) {
 void ensure_xl(nau_ctx* c) {
     c->xl_used = true;  // the next build writes it in its reorder pass
     if (c->xl_rev == c->rebuild_count || c->n == 0) return;
-    k_xl<false><<<blocks_for(c->n), kBlock, 0, c->stream>>>(c->dom, c->n, c->fields[0].d,
-                                                            c->d_key, c->d_xl, nullptr);
+    k_xl<<<std::min(kXlBlocks, blocks_for(c->n)), kBlock, 0, c->stream>>>(
+        c->dom, c->n, c->fields[0].d, c->d_key, c->d_xl, nullptr, nullptr);
     c->launches++;
     c->xl_rev = c->rebuild_count;
 }
@@ -618,7 +640,7 @@ static HalfGrid half_grid(nau_ctx* c, double radius) {
 
 static __global__ void k_publish(const int* src, int* dst) { *(volatile int*)dst = *src; }
 
-bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs) {
+bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs, bool async) {
     const long n = c->n;
     if (n == 0 || !c->use_nlist) return false;
     constexpr int kMaxCap = 1024;  // records per slot; beyond this sweeping is cheaper
@@ -641,6 +663,25 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs) {
         if (cudaMalloc(&c->d_ncount, sizeof(int) * slots) != cudaSuccess) return false;
         c->nc_len = (long)slots;
     }
+    if (async && c->work_len < (long)slots) {
+        if (c->d_work) cudaFree(c->d_work);
+        c->d_work = nullptr;
+        c->work_len = 0;
+        if (cudaMalloc(&c->d_work, sizeof(int) * slots) != cudaSuccess) return false;
+        c->work_len = (long)slots;
+    }
+    if (async && !c->d_nwork && cudaMalloc(&c->d_nwork, sizeof(int)) != cudaSuccess) return false;
+    if (async) {
+        // capacity from the overflow the last build published (mapped memory, no sync):
+        // this build's overflowing slots go to the fallback pass
+        const int seen = *(volatile int*)c->h_nover;
+        if (seen > c->nl_cap) {
+            c->nl_cap = std::min(kMaxCap, ((seen + seen / 4 + 31) / 32) * 32);
+            *(volatile int*)c->h_nover = 0;
+        }
+    }
+    int* wk = async ? c->d_work : nullptr;
+    int* nwk = async ? c->d_nwork : nullptr;
     Geo g = make_geo(c);
     const int T = kSweepThreads;
     const int b = blocks_for(n, T);
@@ -648,10 +689,10 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs) {
     if (!hg.on) {
         ensure_xl(c);
     } else if (c->xl_rev != c->rebuild_count) {
-        // the fp16 path falls back to the fp32 pre-filter when some particle escaped its
-        // cell box (a device flag): fill d_xl on the device in that case only
-        k_xl<true><<<blocks_for(n), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_key,
-                                                             c->d_xl, c->d_hesc);
+        // the fp16 builder falls back to the fp32 pre-filter when some particle escaped
+        // its cell box (a device flag): d_xl filled on the device in that case only
+        k_xl<<<std::min(kXlBlocks, blocks_for(n)), kBlock, 0, c->stream>>>(
+            c->dom, n, c->fields[0].d, c->d_key, c->d_xl, c->d_hesc, nullptr);
         c->launches++;
     }
     for (int attempt = 0; attempt < 3; ++attempt) {
@@ -670,26 +711,27 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs) {
             c->nl_len = need;
         }
         cudaMemsetAsync(c->d_nover, 0, sizeof(int), c->stream);
+        if (async) cudaMemsetAsync(c->d_nwork, 0, sizeof(int), c->stream);
         const double r = radius;
         prof_begin(c, 302);
         if (pairs) {
             const int pb = (int)(((n + 1) / 2 + T - 1) / T);
             switch (c->dom.dim) {
-                case 1: k_nlist_pair<1><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
-                case 2: k_nlist_pair<2><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
-                default: k_nlist_pair<3><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
+                case 1: k_nlist_pair<1><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
+                case 2: k_nlist_pair<2><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
+                default: k_nlist_pair<3><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
             }
         } else if (ordered) {
             switch (c->dom.dim) {
-                case 1: k_nlist<1, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
-                case 2: k_nlist<2, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
-                default: k_nlist<3, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
+                case 1: k_nlist<1, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
+                case 2: k_nlist<2, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
+                default: k_nlist<3, true><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
             }
         } else {
             switch (c->dom.dim) {
-                case 1: k_nlist<1, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
-                case 2: k_nlist<2, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
-                default: k_nlist<3, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg); break;
+                case 1: k_nlist<1, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
+                case 2: k_nlist<2, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
+                default: k_nlist<3, false><<<b, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
             }
         }
         prof_end(c, 302);
@@ -699,6 +741,13 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs) {
         // the previous step's result downloads and stall the step until they finish.
         k_publish<<<1, 1, 0, c->stream>>>(c->d_nover, c->h_nover_dev);
         c->launches++;
+        if (async && hg.on && c->xl_rev != c->rebuild_count) {
+            // the fallback pass sweeps the overflowed slots' candidates with d_xl
+            k_xl<<<std::min(kXlBlocks, blocks_for(n)), kBlock, 0, c->stream>>>(
+                c->dom, n, c->fields[0].d, c->d_key, c->d_xl, c->d_nwork, nullptr);
+            c->launches++;
+        }
+        if (async) return true;  // overflowed slots: count -1, in the worklist
         if (cudaStreamSynchronize(c->stream) != cudaSuccess) return false;
         const int over = *(volatile int*)c->h_nover;
         if (over == 0) return true;
@@ -708,21 +757,23 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs) {
     return false;
 }
 
-int nlist_for(nau_ctx* c, double radius, bool ordered, bool pairs) {
+int nlist_for(nau_ctx* c, double radius, bool ordered, bool pairs, bool async) {
     if (!c->use_nlist || c->n == 0) return 0;
     pairs = pairs && c->use_pairs && !ordered;
+    // an async list may hold overflowed slots: only its own (fallback-aware) consumers reuse it
     if (c->nl_rev == c->rebuild_count && c->nl_radius == radius && c->nl_ordered == ordered &&
-        c->nl_pairs == pairs)
+        c->nl_pairs == pairs && (async || !c->nl_async))
         return pairs ? 2 : 1;
     c->nl_rev = -1;
-    if (!build_nlist(c, radius, ordered, pairs)) {
-        if (!pairs || !build_nlist(c, radius, ordered, false)) return 0;
+    if (!build_nlist(c, radius, ordered, pairs, async)) {
+        if (!pairs || !build_nlist(c, radius, ordered, false, async)) return 0;
         pairs = false;
     }
     c->nl_rev = c->rebuild_count;
     c->nl_radius = radius;
     c->nl_ordered = ordered;
     c->nl_pairs = pairs;
+    c->nl_async = async;
     return pairs ? 2 : 1;
 }
 

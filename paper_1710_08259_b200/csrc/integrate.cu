@@ -106,115 +106,117 @@ struct WcsphArgs {
     DevErr* err;
     NList nl;
     double4* vp;  // (vx, vy, vz, p / (rho * rho)) per slot, written by the density pass
+    const int* work = nullptr;   // the fallback pass: slots whose list overflowed
+    const int* nwork = nullptr;
 };
 
 // Pass 1: rho = sph_S(one, m, one, K, R) (interactions.cpp:40-58 with A = rho = 1),
 //         p = B*((rho/rho0)^gamma - 1).
-template <int DIM, int KF, bool LIST>
+template <int DIM, int KF, bool LIST, bool WORK = false>
 __global__ void __launch_bounds__(kThreads) k_wcsph_density(const __grid_constant__ WcsphArgs a) {
     const Geo& g = a.g;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = k < *g.nact && !is_ghost(g, k);
-    const int kk = valid ? k : 0;
-    const long n = g.n;
-    double xi[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) xi[d] = g.x[d * n + kk];
-    const double radius = a.radius;
-    const double h = 0.5 * radius;
-    const double alpha = kernel_alpha<KF>(a.kdim, h);
-    const double s_unit = a.mass / 1.0;  // m_j / rho_j with the uniform operand rho = 1
-    double acc = 0.0;
-    for_neighbors<DIM, true, LIST>(g, a.xl, a.nl, k, valid, xi, radius, NoLoad{},
-               [&](int, const double* rel, int, NoPayload) {
-        const double dist = norm_rel<DIM>(rel);
-        if (dist > radius) return;
-        const double w = kernel_value<KF>(alpha, h, dist);
-        if (w == 0.0) return;
-        acc = acc + 1.0 * (s_unit * w);
+    for_slots<LIST, WORK>(g, a.nl.count, a.work, a.nwork, [&](const int k, bool valid) {
+        const int kk = valid ? k : 0;
+        const long n = g.n;
+        double xi[3] = {0.0, 0.0, 0.0};
+    #pragma unroll
+        for (int d = 0; d < DIM; ++d) xi[d] = g.x[d * n + kk];
+        const double radius = a.radius;
+        const double h = 0.5 * radius;
+        const double alpha = kernel_alpha<KF>(a.kdim, h);
+        const double s_unit = a.mass / 1.0;  // m_j / rho_j with the uniform operand rho = 1
+        double acc = 0.0;
+        for_neighbors<DIM, true, LIST>(g, a.xl, a.nl, k, valid, xi, radius, NoLoad{},
+                   [&](int, const double* rel, int, NoPayload) {
+            const double dist = norm_rel<DIM>(rel);
+            if (dist > radius) return;
+            const double w = kernel_value<KF>(alpha, h, dist);
+            if (w == 0.0) return;
+            acc = acc + 1.0 * (s_unit * w);
+        });
+        if (!valid) return;
+        const double p = a.B * (pow(acc / a.rho0, a.gamma) - 1.0);
+        if (!isfinite(acc) || !isfinite(p)) latch_error(a.err, 2, kMsgNan, g.orig[k]);
+        a.rho[k] = acc;
+        a.p[k] = p;
+        // the momentum pass's per-neighbour operands in one 32-byte record; p/(rho*rho)
+        // is the reference's per-pair subexpression (interactions.cpp:97), same value
+        double vv[3] = {0.0, 0.0, 0.0};
+    #pragma unroll
+        for (int d = 0; d < DIM; ++d) vv[d] = a.v[d * n + k];
+        a.vp[k] = make_double4(vv[0], vv[1], vv[2], p / (acc * acc));
     });
-    if (!valid) return;
-    const double p = a.B * (pow(acc / a.rho0, a.gamma) - 1.0);
-    if (!isfinite(acc) || !isfinite(p)) latch_error(a.err, 2, kMsgNan, g.orig[k]);
-    a.rho[k] = acc;
-    a.p[k] = p;
-    // the momentum pass's per-neighbour operands in one 32-byte record; p/(rho*rho)
-    // is the reference's per-pair subexpression (interactions.cpp:97), same value
-    double vv[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) vv[d] = a.v[d * n + k];
-    a.vp[k] = make_double4(vv[0], vv[1], vv[2], p / (acc * acc));
 }
 
 // Pass 2: vdot = -1/rho*sph_G11(p,m,rho,K,R) + visc*sph_A(v,m,rho,K,R) + g, one
 // neighbour walk with the two operators' accumulators kept apart.
-template <int DIM, int KF, bool LIST>
+template <int DIM, int KF, bool LIST, bool WORK = false>
 __global__ void __launch_bounds__(kThreads) k_wcsph_momentum(const __grid_constant__ WcsphArgs a) {
     const Geo& g = a.g;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    bool valid = k < *g.nact && !is_ghost(g, k);
-    const int kk = valid ? k : 0;
-    const long n = g.n;
-    double xi[3] = {0.0, 0.0, 0.0}, v_i[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-        xi[d] = g.x[d * n + kk];
-        v_i[d] = a.v[d * n + kk];
-    }
-    const double radius = a.radius;
-    const double h = 0.5 * radius;
-    const double alpha = kernel_alpha<KF>(a.kdim, h);
-    const double m = a.mass;
-    const double rho_i = a.rho[kk];
-    const double p_i = a.p[kk];
-    const int my_orig = g.orig[kk];
-    if (valid && rho_i == 0.0) {
-        latch_error(a.err, 1, kMsgZeroDensity, my_orig);
-        valid = false;
-    }
-    const double pr_i = p_i / (rho_i * rho_i);
-    double G[3] = {0.0, 0.0, 0.0}, A[3] = {0.0, 0.0, 0.0};
-    // per-neighbour operands (v_j, p_j / rho_j^2), gathered ahead of the pair arithmetic
-    const Ld256 load{a.vp};
-    for_neighbors<DIM, true, LIST, false, 2>(g, a.xl, a.nl, k, valid, xi, radius, load,
-               [&](int j, const double* rel, int mask, const double4& pj) {
-        const double dist = norm_rel<DIM>(rel);
-        if (dist > radius) return;
-        if (dist <= 0.0) {  // G11 skips silently; sph_A warns (interactions.cpp:32-38)
-            if (g.orig[j] != my_orig && mask == 0) atomicAdd(&a.err->warnings, 1ull);
-            return;
+    for_slots<LIST, WORK>(g, a.nl.count, a.work, a.nwork, [&](const int k, bool valid) {
+        const int kk = valid ? k : 0;
+        const long n = g.n;
+        double xi[3] = {0.0, 0.0, 0.0}, v_i[3] = {0.0, 0.0, 0.0};
+    #pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+            xi[d] = g.x[d * n + kk];
+            v_i[d] = a.v[d * n + kk];
         }
-        const double sc = kernel_grad_scale<KF>(alpha, h, dist);
-        const double pr_j = pj.w;  // non-finite only if rho_j == 0 or p_j overflowed
-        if (!isfinite(pr_j) && a.rho[j] == 0.0) {
-            latch_error(a.err, 1, kMsgZeroDensity, g.orig[j]);
-            return;
+        const double radius = a.radius;
+        const double h = 0.5 * radius;
+        const double alpha = kernel_alpha<KF>(a.kdim, h);
+        const double m = a.mass;
+        const double rho_i = a.rho[kk];
+        const double p_i = a.p[kk];
+        const int my_orig = g.orig[kk];
+        if (valid && rho_i == 0.0) {
+            latch_error(a.err, 1, kMsgZeroDensity, my_orig);
+            valid = false;
         }
-        const double s = m * (pr_i + pr_j);
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) G[d] = G[d] + (rel[d] * sc) * s;
-        const double vj[3] = {pj.x, pj.y, pj.z};
-        double ap = (mirror_comp(vj[0], 0, DIM, 1, mask, DIM) - v_i[0]) * rel[0];
-#pragma unroll
-        for (int d = 1; d < DIM; ++d)
-            ap = ap + (mirror_comp(vj[d], d, DIM, 1, mask, DIM) - v_i[d]) * rel[d];
-        if (ap >= 0.0) return;
-        const double pi_ij = ap / (rho_i * dist * dist);
-        const double sa = m * pi_ij;
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) A[d] = A[d] + (rel[d] * sc) * sa;
+        const double pr_i = p_i / (rho_i * rho_i);
+        double G[3] = {0.0, 0.0, 0.0}, A[3] = {0.0, 0.0, 0.0};
+        // per-neighbour operands (v_j, p_j / rho_j^2), gathered ahead of the pair arithmetic
+        const Ld256 load{a.vp};
+        for_neighbors<DIM, true, LIST, false, 2>(g, a.xl, a.nl, k, valid, xi, radius, load,
+                   [&](int j, const double* rel, int mask, const double4& pj) {
+            const double dist = norm_rel<DIM>(rel);
+            if (dist > radius) return;
+            if (dist <= 0.0) {  // G11 skips silently; sph_A warns (interactions.cpp:32-38)
+                if (g.orig[j] != my_orig && mask == 0) atomicAdd(&a.err->warnings, 1ull);
+                return;
+            }
+            const double sc = kernel_grad_scale<KF>(alpha, h, dist);
+            const double pr_j = pj.w;  // non-finite only if rho_j == 0 or p_j overflowed
+            if (!isfinite(pr_j) && a.rho[j] == 0.0) {
+                latch_error(a.err, 1, kMsgZeroDensity, g.orig[j]);
+                return;
+            }
+            const double s = m * (pr_i + pr_j);
+    #pragma unroll
+            for (int d = 0; d < DIM; ++d) G[d] = G[d] + (rel[d] * sc) * s;
+            const double vj[3] = {pj.x, pj.y, pj.z};
+            double ap = (mirror_comp(vj[0], 0, DIM, 1, mask, DIM) - v_i[0]) * rel[0];
+    #pragma unroll
+            for (int d = 1; d < DIM; ++d)
+                ap = ap + (mirror_comp(vj[d], d, DIM, 1, mask, DIM) - v_i[d]) * rel[d];
+            if (ap >= 0.0) return;
+            const double pi_ij = ap / (rho_i * dist * dist);
+            const double sa = m * pi_ij;
+    #pragma unroll
+            for (int d = 0; d < DIM; ++d) A[d] = A[d] + (rel[d] * sc) * sa;
+        });
+        if (!valid) return;
+        const double s1 = -1.0 / rho_i;
+        bool bad = false;
+    #pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+            const double gd = rho_i * G[d];
+            const double r = (s1 * gd + a.visc * A[d]) + a.g_acc[d];
+            bad |= !isfinite(r);
+            a.vdot[d * n + k] = r;
+        }
+        if (bad) latch_error(a.err, 2, kMsgNan, my_orig);
     });
-    if (!valid) return;
-    const double s1 = -1.0 / rho_i;
-    bool bad = false;
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-        const double gd = rho_i * G[d];
-        const double r = (s1 * gd + a.visc * A[d]) + a.g_acc[d];
-        bad |= !isfinite(r);
-        a.vdot[d * n + k] = r;
-    }
-    if (bad) latch_error(a.err, 2, kMsgNan, my_orig);
 }
 
 // ---- reductions (fmax/fmin/fsum/fmean), ast.cpp:237-274 ----
@@ -293,6 +295,22 @@ void wcsph_launch_dim(nau_ctx* c, const WcsphArgs& a, int kf, int passes) {
         wcsph_launch<DIM, false>(c, a, kf, passes);
 }
 
+// The fallback pass of an async list build: the overflowed slots swept per particle
+// (the same candidates in the same order as the list).
+template <int DIM>
+void wcsph_fallback(nau_ctx* c, const WcsphArgs& a, int kf, int passes) {
+    constexpr int kBlocks = 148 * 4;
+    if (passes & 1) {
+        if (kf == NAU_K_CUBIC) k_wcsph_density<DIM, NAU_K_CUBIC, false, true><<<kBlocks, kThreads, 0, c->stream>>>(a);
+        else k_wcsph_density<DIM, NAU_K_WENDLAND, false, true><<<kBlocks, kThreads, 0, c->stream>>>(a);
+    }
+    if (passes & 2) {
+        if (kf == NAU_K_CUBIC) k_wcsph_momentum<DIM, NAU_K_CUBIC, false, true><<<kBlocks, kThreads, 0, c->stream>>>(a);
+        else k_wcsph_momentum<DIM, NAU_K_WENDLAND, false, true><<<kBlocks, kThreads, 0, c->stream>>>(a);
+    }
+    c->launches++;
+}
+
 }  // namespace
 
 void launch_commit_if_ok(nau_ctx* c, const double* src, double* dst) {
@@ -345,6 +363,18 @@ void launch_wcsph(nau_ctx* c, const nau_wcsph_params* p, bool lists, int passes)
         case 1: wcsph_launch_dim<1>(c, a, p->kernel_family, passes); break;
         case 2: wcsph_launch_dim<2>(c, a, p->kernel_family, passes); break;
         default: wcsph_launch_dim<3>(c, a, p->kernel_family, passes); break;
+    }
+    if (lists && c->nl_async) {  // slots whose list overflowed: swept per particle
+        WcsphArgs f = a;
+        f.nl.e = nullptr;
+        f.work = c->d_work;
+        f.nwork = c->d_nwork;
+        ensure_xl(c);
+        switch (c->dom.dim) {
+            case 1: wcsph_fallback<1>(c, f, p->kernel_family, passes); break;
+            case 2: wcsph_fallback<2>(c, f, p->kernel_family, passes); break;
+            default: wcsph_fallback<3>(c, f, p->kernel_family, passes); break;
+        }
     }
 }
 

@@ -94,6 +94,30 @@ struct Geo {
 // as neighbours but are not evaluated or integrated.
 __device__ __forceinline__ bool is_ghost(const Geo& g, long k) { return g.upd && !g.upd[k]; }
 
+// The slots one thread block of a per-particle pass evaluates. WORK = false: slot
+// = global thread index, valid below the active count, not a ghost, and (LIST) with a
+// complete neighbour list — a list that overflowed its capacity carries count -1 and
+// its slot is handed to the fallback pass. WORK = true (the fallback pass): the
+// overflow worklist, grid-strided in block-uniform chunks (the sweeps are
+// warp-synchronous, so every lane runs every chunk).
+template <bool LIST, bool WORK, class Body>
+__device__ __forceinline__ void for_slots(const Geo& g, const int* lcount, const int* work,
+                                          const int* nwork, Body&& body) {
+    if constexpr (WORK) {
+        const int nw = *nwork;
+        for (int base = blockIdx.x * blockDim.x; base < nw; base += gridDim.x * blockDim.x) {
+            const int t = base + threadIdx.x;
+            const bool in = t < nw;
+            body(in ? work[t] : 0, in);
+        }
+    } else {
+        const int k = blockIdx.x * blockDim.x + threadIdx.x;
+        bool valid = k < *g.nact && !is_ghost(g, k);
+        if (LIST && valid && lcount[k] < 0) valid = false;  // overflowed: the fallback pass
+        body(k, valid);
+    }
+}
+
 struct FieldBuf {
     int rows = 0, cols = 0;
     double* d = nullptr;    // current storage (cell order)
@@ -407,6 +431,10 @@ struct nau_ctx {
     int mode = NAU_MODE_EXACT;
     int last_wcsph_path = -1;  // nau_wcsph_path: which kernels the last nau_wcsph_step ran
     int wcsph_lists = -1;      // neighbour source of the density pass, reused by the momentum pass
+    int* d_work = nullptr;     // slots whose list overflowed (async list builds) + count
+    int* d_nwork = nullptr;
+    long work_len = 0;
+    bool nl_async = false;     // the cached list may hold overflowed (count -1) entries
     long wcsph_rev = -1;       // ... for this cell build
     int* d_cell_start = nullptr;  // ncells + 2
     int* d_cell_count = nullptr;  // ncells + 1
@@ -423,6 +451,13 @@ struct nau_ctx {
     std::string last_error;
     long last_bad = -1;
     long launches = 0;
+    // CUDA graphs of nau_wcsph_step (capi.cu): captured steps keyed by the host state
+    // they start from (pointers, flags, cache keys, parameters), replayed with that
+    // state's successor applied on the host
+    struct StepGraph;
+    std::vector<StepGraph*> graphs;
+    bool use_graphs = true;
+    int graph_warm = 0;  // uncaptured calls since the last invalidation (allocations settle)
     bool profile = false;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, int>> ev_pairs;  // (class, start event index)
@@ -445,11 +480,15 @@ void launch_build_cells(nau_ctx* c);
 // that may sweep calls this (the paired fp16 list path does not read d_xl).
 void ensure_xl(nau_ctx* c);
 void launch_neighbor_counts(nau_ctx* c, double radius, int* d_out_orig);
-bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs = false);  // false: unusable
+// async: no host synchronisation — an overflowing slot gets count -1 and joins the
+// worklist for the fallback pass (nau_wcsph_pass); capacity grows from the overflow
+// the previous build published.
+bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs = false,
+                 bool async = false);  // false: unusable
 // The current cell build's list for (radius, order, layout), built on first use
 // and shared by every neighbour pass until the cells are rebuilt. Returns 0 (no
 // list: sweep), 1 (per-slot lists) or 2 (paired lists, when `pairs`).
-int nlist_for(nau_ctx* c, double radius, bool ordered, bool pairs = false);
+int nlist_for(nau_ctx* c, double radius, bool ordered, bool pairs = false, bool async = false);
 void launch_unsort(nau_ctx* c, const double* d_src, double* d_dst, int comps);
 void launch_sort_in(nau_ctx* c, const double* d_src_orig, double* d_dst, int comps);
 // interact.cu

@@ -51,7 +51,7 @@ EXPORTS = [
     "nau_case_solve_step", "nau_case_last_error", "nau_wcsph_pass", "nau_select_x", "nau_reserve",
     "nau_rebuild_rows", "nau_histogram_x", "nau_set_ghost_field", "nau_wcsph_pack_rho_p",
     "nau_wcsph_ghost_update", "nau_slab_bounds", "nau_slab_rebalance", "nau_pack_fields",
-    "nau_unpack_fields", "nau_wcsph_ghost_payload",
+    "nau_unpack_fields", "nau_wcsph_ghost_payload", "nau_set_graphs",
 ]
 
 
@@ -181,6 +181,7 @@ def load():
         "nau_pack_fields": (i, [vp, vp, l, vp, i, vp]),
         "nau_unpack_fields": (i, [vp, vp, l, vp, i, vp]),
         "nau_wcsph_ghost_payload": (i, [vp, C.POINTER(WcsphParams)]),
+        "nau_set_graphs": (i, [vp, i]),
         "nau_comm_swap": (i, [vp, vp, l, vp, l, i, vp, vp, vp, vp]),
         "nau_write_vtk": (i, [vp, C.c_char_p, i, vp]),
         "nau_vtk_read": (i, [C.c_char_p, vp]),
@@ -632,6 +633,10 @@ class Context:
 
     def wcsph_step(self, p: WcsphParams):
         self._check(self.L.nau_wcsph_step(self.h, C.byref(p)))
+
+    def set_graphs(self, on):
+        """CUDA-graph replay of wcsph_step (nau_set_graphs; default on)."""
+        self._check(self.L.nau_set_graphs(self.h, 1 if on else 0))
 
     def wcsph_pass(self, p: WcsphParams, k: int):
         """0 cells + list + density/EOS, 1 momentum, 2 symplectic update (nau_wcsph_pass)."""

@@ -1109,3 +1109,34 @@ def test_gravity_shard_path_matches_plain(ctx, fast):
         np.testing.assert_array_equal(ctx2.download(k), ref[k], err_msg=k)
     ctx.set_mode(False)
     ctx2.close()
+
+
+# ------------------------------------------------ graphs / async lists ----
+@pytest.mark.parametrize("fast", [False, True])
+@pytest.mark.parametrize("deck", ["dam3d", "random_overflow"])
+def test_graph_replay_equals_plain_steps(fast, deck):
+    """nau_wcsph_step without host synchronisation and replayed as CUDA graphs after two
+    warm-up calls equals the plain step loop bitwise over 9 steps — including a deck
+    whose neighbour lists overflow (capacity 64 -> grown from the published overflow,
+    overflowed slots swept by the fallback pass) and one above the list cap (every
+    step falls back for the long lists)."""
+    if deck == "dam3d":
+        build = lambda c: _gpu_dam(c, scenes.dam_break(3, dx=0.04))
+    else:
+        build = _random_deck(24000, 2, nau.PERIODIC, 0.25)
+    runs = []
+    for graphs in (False, True):
+        c = nau.Context(0)
+        try:
+            p = build(c)
+            c.set_mode(fast)
+            c.set_graphs(graphs)
+            for _ in range(9):
+                c.wcsph_step(p)
+            c.sync()
+            runs.append(({k: c.download(k) for k in ("r", "rho", "p", "v", "vdot")}, c.active()))
+        finally:
+            c.close()
+    np.testing.assert_array_equal(runs[0][1], runs[1][1])
+    for k in runs[0][0]:
+        np.testing.assert_array_equal(runs[1][0][k], runs[0][0][k], err_msg=k)
