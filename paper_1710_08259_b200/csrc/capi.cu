@@ -973,7 +973,10 @@ nau_status nau_wcsph_pass(nau_ctx* c, const nau_wcsph_params* p, int pass) {
     const bool pairs = c->mode == NAU_MODE_FAST && p->kernel_family == NAU_K_WENDLAND &&
                        p->radius <= min_cs;
     // no host synchronisation: an overflowing list is swept by the fallback pass
-    const int lists = nau::nlist_for(c, p->radius, c->mode == NAU_MODE_EXACT, pairs, true);
+#ifndef NAU_ASYNC_LISTS
+#define NAU_ASYNC_LISTS 1
+#endif
+    const int lists = nau::nlist_for(c, p->radius, c->mode == NAU_MODE_EXACT, pairs, NAU_ASYNC_LISTS);
     {
         int img = 0;
         for (int a = 0; a < c->dom.dim; ++a) img |= c->dom.kind[a] != NAU_CUTOFF;

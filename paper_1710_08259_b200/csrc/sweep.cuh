@@ -787,6 +787,7 @@ __device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __rest
 }
 
 // ---- paired lists (FAST WCSPH deck) -------------------------------------------
+
 // Thread t owns slots 2t and 2t+1. When both sit in one cell (all but ~1 in 64
 // pairs at the BASELINE decks) they share the option sequence, so one record
 // per 32-candidate block carries both survivor masks: (first slot | image code,

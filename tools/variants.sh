@@ -14,8 +14,9 @@ while [ $# -ge 2 ]; do
   ( nvcc $FLAGS $defs -Xptxas -v -c "$CS/fast.cu" -o "$out/fast.o" 2> "$out/fast.ptxas.txt" &&
     nvcc $FLAGS -fmad=false $defs -c "$CS/cells.cu" -o "$out/cells.o" &&
     nvcc $FLAGS -fmad=false $defs -c "$CS/interact.cu" -o "$out/interact.o" &&
-    objs=$(ls $ROOT/build/csrc/*.o | grep -v -e /fast.o -e /cells.o -e /interact.o) &&
-    nvcc $ARCH -shared -o "$out/libnau_b200.so" "$out/fast.o" "$out/cells.o" "$out/interact.o" $objs -lcudart -ldl &&
+    nvcc $FLAGS -fmad=false $defs -c "$CS/capi.cu" -o "$out/capi.o" &&
+    objs=$(ls $ROOT/build/csrc/*.o | grep -v -e /fast.o -e /cells.o -e /interact.o -e /capi.o) &&
+    nvcc $ARCH -shared -o "$out/libnau_b200.so" "$out/fast.o" "$out/cells.o" "$out/interact.o" "$out/capi.o" $objs -lcudart -ldl &&
     echo "built $name" ) &
 done
 wait
