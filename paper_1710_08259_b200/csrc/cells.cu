@@ -365,12 +365,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_nlist(const __grid_constant__
 }
 
 // Paired lists (sweep.cuh consume_pairs): thread t = slots 2t, 2t+1; count[t] =
-// entries of the union of both masks.
+// entries of the union masks, split[t] = first record of the second particle (-1:
+// shared records).
 template <int DIM>
 __global__ void __launch_bounds__(kSweepThreads) k_nlist_pair(const __grid_constant__ Geo g,
                                                               const float4* xl, double radius,
-                                                              uint32_t* list, int* count, int cap,
-                                                              int* over,
+                                                              uint32_t* list, int* count,
+                                                              int* split, int cap, int* over,
                                                               const __grid_constant__ HalfGrid hg,
                                                               int* work, int* nwork) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -381,26 +382,27 @@ __global__ void __launch_bounds__(kSweepThreads) k_nlist_pair(const __grid_const
         count[t] = 0;
         return;
     }
-    uint4* lst = reinterpret_cast<uint4*>(list) + (size_t)(t >> 5) * cap * 32 + (t & 31);
-    int cnt = 0, nrec = 0;
+    uint2* lst = reinterpret_cast<uint2*>(list) + nlist_base(t, cap);
+    int cnt = 0, nrec = 0, sp = -1;
+    const int room = cap - kPairTail;  // the terminator records need two rows
     build_pair_list<DIM>(g, xl, hg, radius, k0, k0 + 1 < nact,
-                         [&](uint32_t v, uint32_t m0, uint32_t m1) {
-        if (m0 | m1) {
-            if (nrec < cap) st_rec4(lst, (unsigned)nrec, v, m0, m1);
-            ++nrec;
-            cnt += __popc(m0 | m1);
-        }
-    });
+                         [&](uint32_t v, uint32_t m) { emit_rec(lst, room, nrec, cnt, v, m); },
+                         [&]() { sp = nrec; });
+    if (nrec <= room) {
+        st_rec(lst, (unsigned)nrec, (uint32_t)k0, 1u);
+        st_rec(lst, (unsigned)nrec + 1u, (uint32_t)k0, 1u);
+        count[t] = cnt;
+        split[t] = sp;
+        return;
+    }
     count[t] = cnt;
-    if (nrec > cap) {
-        atomicMax(over, nrec);
-        if (work) {  // async build: both slots go to the fallback pass
-            count[t] = -1;
-            const bool has1 = k0 + 1 < nact;
-            const int w = atomicAdd(nwork, has1 ? 2 : 1);
-            work[w] = k0;
-            if (has1) work[w + 1] = k0 + 1;
-        }
+    atomicMax(over, nrec + kPairTail);
+    if (work) {  // async build: both slots go to the fallback pass
+        count[t] = -1;
+        const bool has1 = k0 + 1 < nact;
+        const int w = atomicAdd(nwork, has1 ? 2 : 1);
+        work[w] = k0;
+        if (has1) work[w + 1] = k0 + 1;
     }
 }
 
@@ -697,8 +699,8 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs, bool async
     }
     for (int attempt = 0; attempt < 3; ++attempt) {
         // uint2 records + two slack rows (consume_list reads two records ahead);
-        // paired: uint4 records per thread pair + one slack row
-        const size_t need = pairs ? ((size_t)(n + 63) / 64 * 32) * c->nl_cap * 4 + 128
+        // paired: uint2 union records per thread pair, same slack
+        const size_t need = pairs ? ((size_t)(n + 63) / 64 * 32) * c->nl_cap * 2 + 128
                                   : slots * (size_t)c->nl_cap * 2 + 128;
         if (c->nl_len < need) {
             if (c->d_nlist) cudaFree(c->d_nlist);
@@ -717,9 +719,9 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs, bool async
         if (pairs) {
             const int pb = (int)(((n + 1) / 2 + T - 1) / T);
             switch (c->dom.dim) {
-                case 1: k_nlist_pair<1><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
-                case 2: k_nlist_pair<2><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
-                default: k_nlist_pair<3><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->nl_cap, c->d_nover, hg, wk, nwk); break;
+                case 1: k_nlist_pair<1><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->d_ncount + (slots >> 1), c->nl_cap, c->d_nover, hg, wk, nwk); break;
+                case 2: k_nlist_pair<2><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->d_ncount + (slots >> 1), c->nl_cap, c->d_nover, hg, wk, nwk); break;
+                default: k_nlist_pair<3><<<pb, T, 0, c->stream>>>(g, c->d_xl, r, c->d_nlist, c->d_ncount, c->d_ncount + (slots >> 1), c->nl_cap, c->d_nover, hg, wk, nwk); break;
             }
         } else if (ordered) {
             switch (c->dom.dim) {

@@ -631,8 +631,10 @@ __device__ __forceinline__ float half_offset(const AxisOpts& ao, int ci, int o, 
 }
 
 // NP (1 or 2) particles of ONE cell share the option sequence and every
-// coordinate load; each gets its own mask: emit(v, m) with m[NP].
-template <int DIM, bool ORDERED, int NP, class Emit>
+// coordinate load; each gets its own mask: emit(v, m) with m[NP]. UNI (NP = 2):
+// only m[0] = the union of both masks is formed — min(d0, d1) < 0 is one sign
+// test per candidate instead of two.
+template <int DIM, bool ORDERED, int NP, bool UNI = false, class Emit>
 __device__ __forceinline__ void half_scan(const Geo& g, const HalfGrid& hg, const int* ks,
                                           Emit&& emit) {
     const DomainDev& d = g.dom;
@@ -709,6 +711,7 @@ __device__ __forceinline__ void half_scan(const Geo& g, const HalfGrid& hg, cons
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int kw = 4 * u + q;  // word kw: candidates kw, kw + 16
+                    __half2 dp[NP];
 #pragma unroll
                     for (int p = 0; p < NP; ++p) {
                         __half2 dd = nlim2;
@@ -718,7 +721,15 @@ __device__ __forceinline__ void half_scan(const Geo& g, const HalfGrid& hg, cons
                             const __half2 r = __hfma2(o.sg2[a], x2, o.bq2[p][a]);
                             dd = __hfma2(r, r, dd);
                         }
-                        m[p] += (*reinterpret_cast<const uint32_t*>(&dd) & 0x80008000u) >> (15 - kw);
+                        dp[p] = dd;
+                    }
+                    if constexpr (UNI && NP == 2) {
+                        const __half2 dd = __hmin2(dp[0], dp[1]);
+                        m[0] += (*reinterpret_cast<const uint32_t*>(&dd) & 0x80008000u) >> (15 - kw);
+                    } else {
+#pragma unroll
+                        for (int p = 0; p < NP; ++p)
+                            m[p] += (*reinterpret_cast<const uint32_t*>(&dp[p]) & 0x80008000u) >> (15 - kw);
                     }
                 }
             }
@@ -734,7 +745,7 @@ __device__ __forceinline__ void half_scan(const Geo& g, const HalfGrid& hg, cons
             }
             if (o.ns - q0 < 32)
 #pragma unroll
-                for (int p = 0; p < NP; ++p) m[p] &= (1u << (o.ns - q0)) - 1u;
+                for (int p = 0; p < (UNI ? 1 : NP); ++p) m[p] &= (1u << (o.ns - q0)) - 1u;
             emit((uint32_t)(o.s + q0) | o.icode, m);
         }
     }
@@ -750,6 +761,7 @@ struct NList {  // per-step neighbour lists (k_nlist in cells.cu): chunk records
     const uint32_t* e;  // uint2 records (see st_rec), viewed as u32
     const int* count;   // pairs (expanded entries) per slot
     int cap;            // records per slot
+    const int* split = nullptr;  // paired lists: first record of the second particle, or -1
 };
 
 // Record 0 of slot k, in uint2 units (record r is 32 r further).
@@ -789,92 +801,97 @@ __device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __rest
 // ---- paired lists (FAST WCSPH deck) -------------------------------------------
 
 // Thread t owns slots 2t and 2t+1. When both sit in one cell (all but ~1 in 64
-// pairs at the BASELINE decks) they share the option sequence, so one record
-// per 32-candidate block carries both survivor masks: (first slot | image code,
-// m0, m1) as a uint4. The consumer walks the union of the masks; every gathered
-// neighbour (position + payload) serves both particles, each contribution
-// selected by its own bit — the gathers, which bound the per-slot consumers in
-// L1, are shared, and the two particles' arithmetic runs as two independent
-// chains. Pairs that straddle a cell boundary store the first particle's blocks
-// (m1 = 0), then the second's (m0 = 0). Each particle still visits its own
-// candidates in the sweep's order: the same sums as the per-slot lists.
-__device__ __forceinline__ void st_rec4(uint4* base, unsigned r, uint32_t v, uint32_t m0,
-                                        uint32_t m1) {
-    asm volatile(
-        "{\n\t.reg .u64 a;\n\t"
-        "mad.wide.u32 a, %1, 512, %0;\n\t"
-        "st.global.v4.u32 [a], {%2, %3, %4, %5};\n\t}"
-        :
-        : "l"(base), "r"(r), "r"(v), "r"(m0), "r"(m1), "r"(m0 | m1)
-        : "memory");
-}
+// pairs at the BASELINE decks) they share the option sequence, and one 8-byte
+// record per 32-candidate block carries the UNION of their survivor masks. The
+// consumer evaluates every gathered neighbour (position + payload) for both
+// particles as two independent chains: the masks are superset pre-filters, so a
+// candidate only the other particle kept lies beyond the support radius and its
+// contribution is clamped to zero like any other false survivor's. The gathers,
+// which bound the per-slot consumers in L1, are shared, and no per-particle bit
+// is stored or decoded. Pairs that straddle a cell boundary (or a thread whose
+// second slot does not exist) store the first particle's records, then the
+// second's; `split` = the first record of the second particle (-1: shared
+// records), and a particle skips the records it does not own. Each particle
+// still visits its own candidates in the sweep's order: the same sums as the
+// per-slot lists. Two terminator records (own slot, one bit) follow a thread's
+// last record so the consumer's gathers may run two entries past the end.
+constexpr int kPairTail = 2;
 
-// Records of a thread pair; fn(v, m0, m1) per block as in build_list.
-template <int DIM, class Emit2>
+// Records of a thread pair: emit(v, union mask) per block as in build_list;
+// mark() runs between the first particle's records and the second's when they
+// are not shared.
+template <int DIM, class Emit, class Mark>
 __device__ __forceinline__ void build_pair_list(const Geo& g, const float4* __restrict__ xl4,
                                                 const HalfGrid& hg, double radius, int k0,
-                                                bool has1, Emit2&& emit2) {
+                                                bool has1, Emit&& emit, Mark&& mark) {
     const int k1 = k0 + 1;
     if (hg.on && *hg.escaped == 0) {
         if (has1 && g.key[k0] == g.key[k1]) {
             const int ks[2] = {k0, k1};
-            half_scan<DIM, false, 2>(g, hg, ks,
-                                     [&](uint32_t v, const uint32_t* m) { emit2(v, m[0], m[1]); });
+            half_scan<DIM, false, 2, true>(g, hg, ks,
+                                           [&](uint32_t v, const uint32_t* m) { emit(v, m[0]); });
         } else {
-            build_list_half<DIM, false>(g, hg, k0, [&](uint32_t v, uint32_t m) { emit2(v, m, 0u); });
-            if (has1)
-                build_list_half<DIM, false>(g, hg, k1,
-                                            [&](uint32_t v, uint32_t m) { emit2(v, 0u, m); });
+            build_list_half<DIM, false>(g, hg, k0, emit);
+            mark();
+            if (has1) build_list_half<DIM, false>(g, hg, k1, emit);
         }
         return;
     }
     const float pre_r = (float)radius;
-    auto one = [&](int k, bool second) {
-        auto e = [&](uint32_t v, uint32_t m) { second ? emit2(v, 0u, m) : emit2(v, m, 0u); };
+    auto one = [&](int k) {
         if (axis_mode(g, radius) < 2)
-            build_list<DIM, false, false>(g, xl4, k, pre_r, e);
+            build_list<DIM, false, false>(g, xl4, k, pre_r, emit);
         else
-            build_list<DIM, false, true>(g, xl4, k, pre_r, e);
+            build_list<DIM, false, true>(g, xl4, k, pre_r, emit);
     };
-    one(k0, false);
-    if (has1) one(k1, true);
+    one(k0);
+    mark();
+    if (has1) one(k1);
 }
 
-// fn(j, xj_image, image_mask, live0, live1, payload) for the union of the two
-// particles' candidates; IMG = false: no periodic / symmetric axis.
+// fn(j, xj_image, image_mask, dead0, dead1, payload) over the thread's entries;
+// dead_p = ~0 when particle p does not own the entry's record (else 0): the
+// caller ORs it into the word that zeroes the contribution. IMG = false: no
+// periodic / symmetric axis. Entries two past the end are gathered (terminator
+// records) but not evaluated.
 template <int DIM, bool IMG, class Load, class Fn>
-__device__ __forceinline__ void consume_pairs(const Geo& g, const uint4* __restrict__ rec,
-                                              int cnt, Load&& load, Fn&& fn) {
+__device__ __forceinline__ void consume_pairs(const Geo& g, const uint2* __restrict__ rec,
+                                              int cnt, int split, Load&& load, Fn&& fn) {
     constexpr uint32_t kM = (1u << kSlotBits) - 1;
     using P = decltype(load(0));
     struct Buf {
-        uint32_t ent, fl;
+        uint32_t ent;
+        int o0, o1;  // record index relative to the particles' ownership bounds
         double4 p;
         P pl;
     };
-    uint4 cur = rec[0], n1 = rec[32];  // (v, m0, m1, m0 | m1 remaining)
-    int r = 0;
-    auto gen = [&](uint32_t& fl) -> uint32_t {
-        const bool sw = cur.w == 0;
+    uint2 cur = rec[0], n1 = rec[32];
+    const uint2* nx = rec + 64;
+    // particle 0 owns records r < split (o0 < 0), particle 1 records r >= split
+    // (o1 >= 0); shared records: both always
+    int o0 = split < 0 ? -(1 << 30) : -split, o1 = split < 0 ? 0 : -split;
+    auto fetch = [&](Buf& b) {
+        const bool sw = cur.y == 0;
         cur.x = sw ? n1.x : cur.x;
         cur.y = sw ? n1.y : cur.y;
-        cur.z = sw ? n1.z : cur.z;
-        cur.w = sw ? n1.w : cur.w;
-        r += sw;
-        if (sw) n1 = rec[(r + 1) * 32];  // at most record `nrec`: the slack row
-        const uint32_t b = (uint32_t)(__ffs(cur.w) - 1);
-        cur.w &= cur.w - 1;
-        fl = ((cur.y >> b) & 1u) | (((cur.z >> b) & 1u) << 1);
-        return cur.x + b;
-    };
-    auto fetch = [&](Buf& b, int s) {
-        b.fl = 0;
-        b.ent = s < cnt ? gen(b.fl) : 0u;
-        b.p = ld256(g.p4 + (b.ent & kM));
-        b.pl = load((int)(b.ent & kM));
+        o0 += sw;
+        o1 += sw;
+        if (sw) {
+            n1 = *nx;  // at most two records past the terminators: inside the slack row
+            nx += 32;
+        }
+        const uint32_t bit = (uint32_t)(__ffs(cur.y) - 1);
+        cur.y &= cur.y - 1;
+        b.ent = cur.x + bit;
+        b.o0 = o0;
+        b.o1 = o1;
+        // !IMG: every image code is 0, the entry is the slot
+        const uint32_t slot = IMG ? (b.ent & kM) : b.ent;
+        b.p = ld256(g.p4 + slot);
+        b.pl = load((int)slot);
     };
     auto process = [&](const Buf& b) {
-        const int j = (int)(b.ent & kM);
+        const int j = (int)(IMG ? (b.ent & kM) : b.ent);
         double xj[3] = {b.p.x, b.p.y, b.p.z};
         int mask = 0;
         if constexpr (IMG) {
@@ -888,16 +905,19 @@ __device__ __forceinline__ void consume_pairs(const Geo& g, const uint4* __restr
                 }
             }
         }
-        fn(j, xj, mask, (b.fl & 1u) != 0, (b.fl & 2u) != 0, b.pl);
+        fn(j, xj, mask, ~(unsigned)(b.o0 >> 31), (unsigned)(b.o1 >> 31), b.pl);
     };
     Buf A, B;
-    fetch(A, 0);
-    for (int s = 0; s < cnt; s += 2) {
-        fetch(B, s + 1);
+    fetch(A);
+    fetch(B);
+    int s = 0;
+    for (; s + 2 <= cnt; s += 2) {
         process(A);
-        fetch(A, s + 2);
-        process(B);  // past the end: fl = 0, both contributions deselected
+        fetch(A);
+        process(B);
+        fetch(B);
     }
+    if (s < cnt) process(A);
 }
 
 }  // namespace nau
