@@ -492,6 +492,13 @@ long nau_launch_count(nau_ctx* ctx);
 enum { NAU_PATH_IMAGES = 1, NAU_PATH_FAST = 16 };
 int nau_wcsph_path(nau_ctx* ctx);
 
+/* Instrumentation: shape of the cached neighbour lists (synchronises). out[0] =
+ * list-walking threads (one per particle, or per particle pair with paired lists),
+ * out[1] = entries they walk in total, out[2] = entries a warp-synchronous walk costs
+ * (32 x the longest list of each warp, summed): out[1] / out[2] is the consumers'
+ * lane efficiency. NAU_ERR_ARG when no list is cached. */
+nau_status nau_list_stats(nau_ctx* ctx, double out[3]);
+
 /* Microbenchmark: measured fp64 FMA throughput (TFLOP/s) of this GPU. */
 double nau_fp64_peak_tflops(int device);
 

@@ -1293,4 +1293,30 @@ long nau_launch_count(nau_ctx* c) { return c->launches; }
 
 int nau_wcsph_path(nau_ctx* c) { return c ? c->last_wcsph_path : -1; }
 
+nau_status nau_list_stats(nau_ctx* c, double out[3]) {
+    if (!c || !out) return NAU_ERR_ARG;
+    if (c->nl_rev != c->rebuild_count || !c->d_ncount || c->n == 0)
+        return fail(c, NAU_ERR_ARG, "no neighbour list is cached");
+    const long threads = c->nl_pairs ? (c->n + 1) / 2 : c->n;
+    std::vector<int> cnt((size_t)threads);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess ||
+        cudaMemcpy(cnt.data(), c->d_ncount, sizeof(int) * (size_t)threads, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return fail(c, NAU_ERR_CUDA, "list statistics: copy failed");
+    double walkers = 0, entries = 0, cost = 0;
+    for (long w = 0; w < threads; w += 32) {
+        int mx = 0;
+        for (long t = w; t < std::min(threads, w + 32); ++t) {
+            if (cnt[(size_t)t] <= 0) continue;  // ghosts / overflowed slots: not walked
+            walkers += 1;
+            entries += cnt[(size_t)t];
+            mx = std::max(mx, cnt[(size_t)t]);
+        }
+        cost += 32.0 * mx;
+    }
+    out[0] = walkers;
+    out[1] = entries;
+    out[2] = cost;
+    return NAU_OK;
+}
+
 }  // extern "C"

@@ -816,6 +816,10 @@ __device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __rest
 // per-slot lists. Two terminator records (own slot, one bit) follow a thread's
 // last record so the consumer's gathers may run two entries past the end.
 constexpr int kPairTail = 2;
+#ifndef NAU_REC_PF
+#define NAU_REC_PF 0
+#endif
+constexpr int kPairSlackRows = 1 + NAU_REC_PF;  // rows a consumer may touch past a group's last
 
 // Records of a thread pair: emit(v, union mask) per block as in build_list;
 // mark() runs between the first particle's records and the second's when they
@@ -878,6 +882,11 @@ __device__ __forceinline__ void consume_pairs(const Geo& g, const uint2* __restr
         o1 += sw;
         if (sw) {
             n1 = *nx;  // at most two records past the terminators: inside the slack row
+#if NAU_REC_PF
+            // the records stream from DRAM once: pull the row NAU_REC_PF switches ahead
+            // toward L1 (one record ahead hides ~300 cycles of a ~800-cycle latency)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(nx + 32 * NAU_REC_PF));
+#endif
             nx += 32;
         }
         const uint32_t bit = (uint32_t)(__ffs(cur.y) - 1);
@@ -886,7 +895,11 @@ __device__ __forceinline__ void consume_pairs(const Geo& g, const uint2* __restr
         b.o0 = o0;
         b.o1 = o1;
         // !IMG: every image code is 0, the entry is the slot
+#ifdef NAU_PROBE_L1HIT  // timing probe only (wrong results): every gather hits L1
+        const uint32_t slot = b.ent & 1023u;
+#else
         const uint32_t slot = IMG ? (b.ent & kM) : b.ent;
+#endif
         b.p = ld256(g.p4 + slot);
         b.pl = load((int)slot);
     };

@@ -37,7 +37,7 @@ EXPORTS = [
     "nau_build_cells", "nau_cells_dirty", "nau_rebuild_count", "nau_warning_count", "nau_ncells",
     "nau_cell_tables", "nau_neighbor_counts", "nau_interact", "nau_interact_g11_l0", "nau_euler", "nau_symplectic_step",
     "nau_wcsph_step", "nau_reduce", "nau_sync", "nau_last_error", "nau_profile_enable",
-    "nau_profile_ms", "nau_launch_count", "nau_wcsph_path", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
+    "nau_profile_ms", "nau_launch_count", "nau_wcsph_path", "nau_list_stats", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
     "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows", "nau_dem_step",
     "nau_leapfrog_step", "nau_pack_sources", "nau_gravity_sources", "nau_set_neighbor_lists",
     "nau_upload_async", "nau_download_async", "nau_io_fence", "nau_io_join", "nau_eval",
@@ -151,6 +151,7 @@ def load():
         "nau_profile_ms": (d, [vp, i, C.POINTER(l)]),
         "nau_launch_count": (l, [vp]),
         "nau_wcsph_path": (i, [vp]),
+        "nau_list_stats": (i, [vp, C.POINTER(d)]),
         "nau_fp64_peak_tflops": (d, [i]),
         "nau_set_mode": (i, [vp, i]),
         "nau_get_mode": (i, [vp]),
@@ -669,6 +670,15 @@ class Context:
     @property
     def launches(self):
         return self.L.nau_launch_count(self.h)
+
+    def list_stats(self):
+        """dict(walkers, entries, warp_cost, lane_efficiency) of the cached neighbour
+        lists (nau_list_stats; synchronises)."""
+        out = (C.c_double * 3)()
+        self._check(self.L.nau_list_stats(self.h, out))
+        return {"walkers": out[0], "entries": out[1], "warp_cost": out[2],
+                "entries_per_walker": out[1] / max(out[0], 1.0),
+                "lane_efficiency": out[1] / max(out[2], 1.0)}
 
     @property
     def wcsph_path(self):
