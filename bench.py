@@ -505,9 +505,10 @@ class Gravity(Workload):
 
 class GravityShard(Gravity):
     """cfg4 sharded over the ranks: each rank owns N/W bodies (a
-    contiguous block of the global order); positions + masses are all-gathered
-    (NCCL) every step and every rank evaluates its bodies against all sources in
-    global order — identical sums to the single-GPU run."""
+    contiguous block of the global order); every step each rank's positions + masses
+    reach all ranks as chunk `rank` of a broadcast pipeline (NCCL; slab.pipelined_sources:
+    chunk c + 1 in flight while chunk c is evaluated) and every rank sums its bodies
+    against the chunks in global order — identical sums to the single-GPU run."""
 
     def __init__(self, dist):
         super().__init__()
@@ -531,7 +532,7 @@ class GravityShard(Gravity):
         self.ctx = ctx
         self.dev = f"cuda:{torch.cuda.current_device()}"
         self.local_rows = torch.empty((nl, 4), dtype=torch.float64, device=self.dev)
-        self.all_rows = torch.empty((N, 4), dtype=torch.float64, device=self.dev)
+        self.src_bufs = [torch.empty((nl, 4), dtype=torch.float64, device=self.dev) for _ in range(2)]
         self.N, self.nl = N, nl
         self.fv, self.fa = ctx.fields["v"].id, ctx.fields["a"].id
         self._forces()  # a(t = 0)
@@ -548,15 +549,23 @@ class GravityShard(Gravity):
         import torch
         ctx, prm = self.ctx, self.sc.params
         ctx._check(ctx.L.nau_pack_sources(ctx.h, -1, prm["m"], self.local_rows.data_ptr()))
-        if self.dist.world > 1:
-            ctx.sync()
-            self.dist.pg.all_gather_into_tensor(self.all_rows, self.local_rows)
-            torch.cuda.current_stream().synchronize()
-            src = self.all_rows
-        else:
-            src = self.local_rows
-        ctx._check(ctx.L.nau_gravity_sources(ctx.h, src.data_ptr(), self.N, self.g0, prm["G"],
-                                             prm["eps"], self.fa))
+        if self.dist.world == 1:
+            ctx._check(ctx.L.nau_gravity_sources(ctx.h, self.local_rows.data_ptr(), self.N, self.g0,
+                                                 prm["G"], prm["eps"], self.fa))
+            return
+        # broadcast-pipelined sources: chunk c + 1 is in flight while chunk c is evaluated,
+        # chunks consumed in global order (= the single-GPU sums), no host synchronisation
+        from paper_1710_08259_b200 import slab
+        stream = torch.cuda.ExternalStream(ctx.L.nau_get_stream(ctx.h))
+        nl = self.nl
+
+        def consume(c, rows):
+            ctx._check(ctx.L.nau_gravity_sources_part(ctx.h, rows.data_ptr(), nl, self.g0 - c * nl,
+                                                      prm["G"], prm["eps"], self.fa, int(c > 0)))
+
+        with torch.cuda.stream(stream):  # transfers are ordered after the pack, kernels after them
+            slab.pipelined_sources(self.dist.pg, self.local_rows, self.src_bufs, self.dist.world,
+                                   self.dist.rank, consume)
 
     def step(self, ctx):
         dt = self.sc.params["dt"]

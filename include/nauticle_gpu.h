@@ -254,6 +254,14 @@ nau_status nau_leapfrog_step(nau_ctx* ctx, const nau_gravity_params* prm);
 nau_status nau_pack_sources(nau_ctx* ctx, int f_m, double m, double* dev_rows);
 nau_status nau_gravity_sources(nau_ctx* ctx, const double* dev_src, long nsrc, long self_off,
                                double G, double eps, int out_field);
+/* One chunk of the sources: with accumulate != 0 the sums continue from the values
+ * already in out_field, so chunks evaluated in global order (0, 1, ...) give the sums
+ * of one nau_gravity_sources call over all of them bit for bit. self_off is relative
+ * to the chunk (local body k is the chunk's source self_off + k; out of range: none).
+ * Lets the host overlap the transfer of chunk c + 1 with the pair loop over chunk c
+ * (the all-gather "can be ring-pipelined with compute"). */
+nau_status nau_gravity_sources_part(nau_ctx* ctx, const double* dev_src, long nsrc, long self_off,
+                                    double G, double eps, int out_field, int accumulate);
 
 /* ≙ ReductionNode fsum/fmax/fmin/fmean over active particles (sfl/ast.cpp:237-274).
  * kind: 0 max, 1 min, 2 sum, 3 mean; out has rows*cols doubles (max/min: 1). */

@@ -290,15 +290,33 @@ __global__ void k_reorder(DomainDev d, long n, const int* perm, const int* orig,
     key_s[s] = kk;
     active_s[s] = active[k];
     const bool act = kk < d.ncells;
-    for (int f = 0; f < t.nf; ++f) {
+    // positions first (field 0), then the other fields with each field's component
+    // loads issued together before its stores (non-coherent loads: the compiler
+    // cannot prove src and dst distinct, and a load -> store chain per component
+    // leaves one gather in flight per thread)
+    double x[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) x[a] = __ldg(t.src[0] + a * n + k);
+    if (!(act && (t.skip & 1ULL))) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) t.dst[0][a * n + s] = x[a];
+        for (int c = DIM; c < t.comps[0]; ++c) t.dst[0][c * n + s] = __ldg(t.src[0] + c * n + k);
+    }
+    for (int f = 1; f < t.nf; ++f) {
         if (act && ((t.skip >> f) & 1ULL)) continue;
         const double* src = t.src[f];
         double* dst = t.dst[f];
-        for (int c = 0; c < t.comps[f]; ++c) dst[c * n + s] = src[c * n + k];
-    }
-    double x[3] = {0.0, 0.0, 0.0};
+        const int nc = t.comps[f];
+        for (int c0 = 0; c0 < nc; c0 += 4) {
+            double v[4];
 #pragma unroll
-    for (int a = 0; a < DIM; ++a) x[a] = t.src[0][a * n + k];
+            for (int u = 0; u < 4; ++u)
+                if (c0 + u < nc) v[u] = __ldg(src + (c0 + u) * n + k);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c0 + u < nc) dst[(c0 + u) * n + s] = v[u];
+        }
+    }
     if (xl) {
         float4 p = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
         if (act) {

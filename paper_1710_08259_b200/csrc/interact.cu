@@ -379,6 +379,7 @@ struct GravArgs {
     // local body k is source self_off + k; m = 0 marks an inactive source
     const double4* src;
     long nsrc, self_off;
+    int accumulate;  // start from the sums in `out` (a later chunk of the sources)
 };
 
 // FAST: s = G m_j rsqrt(r2)^3 with FMA (≈1e-15 relative per pair); exact: G m_j / (r2 sqrt r2).
@@ -400,6 +401,9 @@ __global__ void __launch_bounds__(kGravTile) k_gravity(const __grid_constant__ G
     }
     const double eps2 = eps * eps;
     double acc[3] = {0.0, 0.0, 0.0};
+    if (mine && a.accumulate)
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) acc[d] = a.out[d * n + k];
     bool coincident = false;
     const long ns = a.src ? a.nsrc : n;
     const long self = a.self_off + k;
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(kGravThreads) k_gravity_fast(const __grid_cons
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             xi[b][d] = (d < DIM && k < n) ? a.x[d * n + k] : 0.0;
-            acc[b][d] = 0.0;
+            acc[b][d] = (a.accumulate && d < DIM && k < n) ? a.out[d * n + k] : 0.0;
         }
     }
     const long ns = a.src ? a.nsrc : n;
@@ -656,6 +660,7 @@ void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int n
         a.src = gsrc ? gsrc->src : nullptr;
         a.nsrc = gsrc ? gsrc->nsrc : 0;
         a.self_off = gsrc ? gsrc->self_off : 0;
+        a.accumulate = gsrc ? gsrc->accumulate : 0;
         const int blocks = (int)((c->n + kGravTile - 1) / kGravTile);
         prof_begin(c, 100 + op);
         const bool fast = c->mode == NAU_MODE_FAST;

@@ -495,6 +495,7 @@ void launch_sort_in(nau_ctx* c, const double* d_src_orig, double* d_dst, int com
 struct GravSources {  // all-gathered (x, y, z, m) rows for sharded n-body
     const double4* src;
     long nsrc, self_off;
+    int accumulate = 0;  // continue the sums already in the output (source chunks in order)
 };
 void launch_interact(nau_ctx* c, int op, int kf, int kdim, const Opd* ops, int nops,
                      double* out, int out_rows, int out_cols, int a_rows, int a_cols,

@@ -331,6 +331,11 @@ nau_status nau_pack_sources(nau_ctx* c, int f_m, double m, double* dev_rows) {
 
 nau_status nau_gravity_sources(nau_ctx* c, const double* dev_src, long nsrc, long self_off,
                                double G, double eps, int out_field) {
+    return nau_gravity_sources_part(c, dev_src, nsrc, self_off, G, eps, out_field, 0);
+}
+
+nau_status nau_gravity_sources_part(nau_ctx* c, const double* dev_src, long nsrc, long self_off,
+                                    double G, double eps, int out_field, int accumulate) {
     if (c->fields.empty() || out_field <= 0 || out_field >= (int)c->fields.size() ||
         !c->fields[out_field].live || c->fields[out_field].comps() != c->dom.dim)
         return NAU_ERR_ARG;
@@ -341,7 +346,7 @@ nau_status nau_gravity_sources(nau_ctx* c, const double* dev_src, long nsrc, lon
     }
     ops[1].v[0] = G;
     ops[2].v[0] = eps;
-    nau::GravSources gs{reinterpret_cast<const double4*>(dev_src), nsrc, self_off};
+    nau::GravSources gs{reinterpret_cast<const double4*>(dev_src), nsrc, self_off, accumulate};
     const int dim = c->dom.dim;
     nau::launch_interact(c, NAU_OP_GRAVITY, 0, 0, ops, 3, c->fields[out_field].d, dim, 1, 1, 1,
                          nullptr, &gs);

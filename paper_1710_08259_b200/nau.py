@@ -39,7 +39,7 @@ EXPORTS = [
     "nau_wcsph_step", "nau_reduce", "nau_sync", "nau_last_error", "nau_profile_enable",
     "nau_profile_ms", "nau_launch_count", "nau_wcsph_path", "nau_list_stats", "nau_fp64_peak_tflops", "nau_set_mode", "nau_get_mode",
     "nau_row_width", "nau_select", "nau_pack_rows", "nau_load_rows", "nau_dem_step",
-    "nau_leapfrog_step", "nau_pack_sources", "nau_gravity_sources", "nau_set_neighbor_lists",
+    "nau_leapfrog_step", "nau_pack_sources", "nau_gravity_sources", "nau_gravity_sources_part", "nau_set_neighbor_lists",
     "nau_upload_async", "nau_download_async", "nau_io_fence", "nau_io_join", "nau_eval",
     "nau_set_random_state", "nau_get_random_counters", "nau_comm_unique_id", "nau_comm_init",
     "nau_comm_destroy", "nau_slab_config", "nau_migrate", "nau_halo_exchange", "nau_comm_swap",
@@ -163,6 +163,7 @@ def load():
         "nau_leapfrog_step": (i, [vp, C.POINTER(GravityParams)]),
         "nau_pack_sources": (i, [vp, i, d, vp]),
         "nau_gravity_sources": (i, [vp, vp, l, l, d, d, i]),
+        "nau_gravity_sources_part": (i, [vp, vp, l, l, d, d, i, i]),
         "nau_set_neighbor_lists": (i, [vp, i]),
         "nau_upload_async": (i, [vp, i, vp, l]),
         "nau_download_async": (i, [vp, i, vp, l]),

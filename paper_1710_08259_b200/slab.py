@@ -442,3 +442,31 @@ class GpuBackend:
 
     def take(self, rows, mask):
         return rows[self.torch.as_tensor(np.asarray(mask, bool), device=rows.device)]
+
+
+# ------------------------------------------------------- sharded n-body sources ----
+def pipelined_sources(dist, local_rows, bufs, world: int, rank: int, consume, wait=None):
+    """Sharded all-pairs schedule: instead of one all-gather
+    followed by the whole pair loop, rank c broadcasts its (x, y, z, m) rows as chunk c
+    while every rank evaluates chunk c - 1 — the transfer of each chunk hides behind the
+    pair loop over the previous one. Chunks are consumed in GLOBAL order 0..world-1 on
+    every rank (`consume(c, rows)`, which continues the sums: nau_gravity_sources_part),
+    so the result equals the single-GPU sum order bit for bit.
+
+    `bufs`: two receive tensors shaped like `local_rows`; the broadcasts are asynchronous
+    (`async_op=True`), `wait(work)` orders the consumer's stream after a transfer
+    (default: work.wait(), which NCCL turns into a stream dependency, not a host block).
+    """
+    wait = wait or (lambda w: w.wait())
+
+    def post(c):
+        t = local_rows if c == rank else bufs[c & 1]
+        return t, dist.broadcast(t, src=c, async_op=True)
+
+    nxt = post(0)
+    for c in range(world):
+        rows, work = nxt
+        wait(work)
+        if c + 1 < world:
+            nxt = post(c + 1)  # lands in the other buffer while chunk c is evaluated
+        consume(c, rows)

@@ -1111,6 +1111,33 @@ def test_gravity_shard_path_matches_plain(ctx, fast):
     ctx2.close()
 
 
+@pytest.mark.parametrize("fast", [False, True])
+def test_gravity_source_chunks_continue_the_sums(ctx, fast):
+    """nau_gravity_sources_part over 4 source chunks in global order (what the broadcast
+    pipeline of the sharded step consumes) = one nau_gravity_sources call, bitwise."""
+    import torch
+    sc = scenes.plummer(n=2048)
+    prm = sc.params
+    ctx.set_mode(fast)
+    ctx.set_domain(3, sc.min_cells, sc.max_cells, sc.cell_size, sc.kinds)
+    ctx.set_particles(sc.pos)
+    ctx.add_field("a", 3, 1, 0.0)
+    ctx.add_field("b", 3, 1, 0.0)
+    ctx.boundary_shift()
+    rows = torch.empty((sc.n, 4), dtype=torch.float64, device="cuda:0")
+    ctx._check(ctx.L.nau_pack_sources(ctx.h, -1, prm["m"], rows.data_ptr()))
+    fa, fb = ctx.fields["a"].id, ctx.fields["b"].id
+    ctx._check(ctx.L.nau_gravity_sources(ctx.h, rows.data_ptr(), sc.n, 0, prm["G"], prm["eps"], fa))
+    nc = sc.n // 4
+    for c in range(4):
+        chunk = rows[c * nc:(c + 1) * nc]
+        ctx._check(ctx.L.nau_gravity_sources_part(ctx.h, chunk.data_ptr(), nc, -c * nc, prm["G"],
+                                                  prm["eps"], fb, int(c > 0)))
+    ctx.sync()
+    np.testing.assert_array_equal(ctx.download("b"), ctx.download("a"))
+    ctx.set_mode(False)
+
+
 # ------------------------------------------------ graphs / async lists ----
 @pytest.mark.parametrize("fast", [False, True])
 @pytest.mark.parametrize("deck", ["dam3d", "random_overflow"])
