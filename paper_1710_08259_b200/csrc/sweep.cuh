@@ -817,7 +817,7 @@ __device__ __forceinline__ void for_neighbors(const Geo& g, const float4* __rest
 // last record so the consumer's gathers may run two entries past the end.
 constexpr int kPairTail = 2;
 #ifndef NAU_REC_PF
-#define NAU_REC_PF 0
+#define NAU_REC_PF 4  // record prefetch distance of the momentum consumer
 #endif
 constexpr int kPairSlackRows = 1 + NAU_REC_PF;  // rows a consumer may touch past a group's last
 
@@ -858,7 +858,9 @@ __device__ __forceinline__ void build_pair_list(const Geo& g, const float4* __re
 // caller ORs it into the word that zeroes the contribution. IMG = false: no
 // periodic / symmetric axis. Entries two past the end are gathered (terminator
 // records) but not evaluated.
-template <int DIM, bool IMG, class Load, class Fn>
+// PF > 0: each record switch also pulls the row PF switches ahead toward L1 (the
+// records stream from DRAM once; measured at cfg2: momentum -2.4%, density +2.7%).
+template <int DIM, bool IMG, int PF = 0, class Load, class Fn>
 __device__ __forceinline__ void consume_pairs(const Geo& g, const uint2* __restrict__ rec,
                                               int cnt, int split, Load&& load, Fn&& fn) {
     constexpr uint32_t kM = (1u << kSlotBits) - 1;
@@ -882,11 +884,7 @@ __device__ __forceinline__ void consume_pairs(const Geo& g, const uint2* __restr
         o1 += sw;
         if (sw) {
             n1 = *nx;  // at most two records past the terminators: inside the slack row
-#if NAU_REC_PF
-            // the records stream from DRAM once: pull the row NAU_REC_PF switches ahead
-            // toward L1 (one record ahead hides ~300 cycles of a ~800-cycle latency)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(nx + 32 * NAU_REC_PF));
-#endif
+            if constexpr (PF > 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(nx + 32 * PF));
             nx += 32;
         }
         const uint32_t bit = (uint32_t)(__ffs(cur.y) - 1);
