@@ -723,13 +723,22 @@ __device__ __forceinline__ void half_scan(const Geo& g, const HalfGrid& hg, cons
                         }
                         dp[p] = dd;
                     }
+                    // the two sign bits enter at bits 15 / 31 and every later word rotates
+                    // them one place down: word kw ends at bits kw, kw + 16 (a rotate and
+                    // one bit-select per word instead of mask, shift, add)
+                    auto push = [](uint32_t m, const __half2& dd) {
+                        m = __funnelshift_r(m, m, 1);
+                        uint32_t r;  // (m & ~K) | (bits & K), K = the sign bits: one LOP3
+                        asm("lop3.b32 %0, %1, %2, 0x80008000, 0xD8;"
+                            : "=r"(r)
+                            : "r"(m), "r"(*reinterpret_cast<const uint32_t*>(&dd)));
+                        return r;
+                    };
                     if constexpr (UNI && NP == 2) {
-                        const __half2 dd = __hmin2(dp[0], dp[1]);
-                        m[0] += (*reinterpret_cast<const uint32_t*>(&dd) & 0x80008000u) >> (15 - kw);
+                        m[0] = push(m[0], __hmin2(dp[0], dp[1]));
                     } else {
 #pragma unroll
-                        for (int p = 0; p < NP; ++p)
-                            m[p] += (*reinterpret_cast<const uint32_t*>(&dp[p]) & 0x80008000u) >> (15 - kw);
+                        for (int p = 0; p < NP; ++p) m[p] = push(m[p], dp[p]);
                     }
                 }
             }
