@@ -276,7 +276,7 @@ struct ReorderTable {
 // consumers), and when requested the fp32 pre-filter copy xl and the fp16
 // cell-relative coordinates of the list builder (no separate pass over r).
 template <int DIM>
-__global__ void k_reorder(DomainDev d, long n, const int* perm, const int* orig, const int* key,
+__global__ void __launch_bounds__(kBlock, 6) k_reorder(DomainDev d, long n, const int* perm, const int* orig, const int* key,
                           const uint8_t* active, int* orig_s, int* key_s, uint8_t* active_s,
                           float4* xl, double4* p4, const int* skey, int* skey_s,
                           ReorderTable t, HalfOut ho, const int* cell_start,
