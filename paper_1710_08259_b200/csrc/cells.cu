@@ -719,7 +719,7 @@ bool build_nlist(nau_ctx* c, double radius, bool ordered, bool pairs, bool async
         // uint2 records + two slack rows (consume_list reads two records ahead);
         // paired: uint2 union records per thread pair, same slack
         const size_t need = pairs ? ((size_t)(n + 63) / 64 * 32) * c->nl_cap * 2 + 64 * (kPairSlackRows + 1)
-                                  : slots * (size_t)c->nl_cap * 2 + 128;
+                                  : slots * (size_t)c->nl_cap * 2 + 64 * (2 + NAU_LIST_PF);
         if (c->nl_len < need) {
             if (c->d_nlist) cudaFree(c->d_nlist);
             c->d_nlist = nullptr;

@@ -445,6 +445,9 @@ __device__ __forceinline__ void build_list(const Geo& g, const float4* __restric
 #ifndef NAU_GEN_SELECT
 #define NAU_GEN_SELECT 1
 #endif
+#ifndef NAU_LIST_PF
+#define NAU_LIST_PF 4
+#endif
 template <int DIM, bool AXIS, bool FAST, int NB, bool IMG = true, class Load, class Fn>
 __device__ __forceinline__ void consume_list(const Geo& g, const uint2* __restrict__ rec, int cnt,
                                              const double* xi, Load&& load, Fn&& fn) {
@@ -467,7 +470,14 @@ __device__ __forceinline__ void consume_list(const Geo& g, const uint2* __restri
         n1.x = sw ? n2.x : n1.x;
         n1.y = sw ? n2.y : n1.y;
         r += sw;
-        if (sw) n2 = rec[(r + 2) * 32];
+        if (sw) {
+            n2 = rec[(r + 2) * 32];
+#if NAU_LIST_PF
+            // sparse records switch every 1-2 entries and stream from DRAM: pull the
+            // row NAU_LIST_PF switches ahead toward L1 (slack rows cover the overrun)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + (r + 2 + NAU_LIST_PF) * 32));
+#endif
+        }
 #else
         if (cur.y == 0) {
             cur = n1;
