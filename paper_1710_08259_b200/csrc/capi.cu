@@ -76,6 +76,7 @@ void free_particles(nau_ctx* c) {
     dfree(c->d_okey);
     dfree(c->d_xl);
     dfree(c->d_aux);
+    dfree(c->d_pk);
     dfree(c->d_p4);
     dfree(c->d_skey);
     dfree(c->d_skey_s);

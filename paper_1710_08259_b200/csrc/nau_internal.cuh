@@ -378,6 +378,7 @@ struct nau_ctx {
     int* d_skey_s = nullptr;
     float4* d_xl = nullptr;  // fp32 global-origin coordinates (sweep pre-filters)
     double4* d_aux = nullptr;  // per-particle scratch (fast WCSPH: v and p / rho^2 packed)
+    double4* d_pk = nullptr;   // (A, m, 1/rho, rho) of the scalar-A SPH rules (fast.cu), lazily
     double4* d_p4 = nullptr;  // packed positions (written by the reorder pass)
     int* d_sel = nullptr;     // nau_select block-count scratch
     long sel_len = 0;
