@@ -1138,6 +1138,29 @@ def test_gravity_source_chunks_continue_the_sums(ctx, fast):
     ctx.set_mode(False)
 
 
+def test_list_stats_of_the_paired_lists():
+    """nau_list_stats on the FAST dam-break deck: one walker per particle pair, the union
+    lists hold every neighbour of both particles (entries >= the larger neighbour count,
+    <= their sum) and the warp-wide walk loses little to uneven lists."""
+    c = nau.Context(0)
+    try:
+        sc = scenes.dam_break(3, dx=0.04)
+        p = _gpu_dam(c, sc)
+        c.set_mode(True)
+        c.wcsph_step(p)
+        c.sync()
+        assert c.wcsph_path["source"] == "paired"
+        c.wcsph_pass(p, 0)  # the lists of the current positions
+        st = c.list_stats()
+        counts = c.neighbor_counts(sc.params["radius"])
+        n_act = int(c.active().sum())
+        assert st["walkers"] == (n_act + 1) // 2
+        assert counts.sum() / 2.0 <= st["entries"] <= counts.sum() * 1.02
+        assert 0.8 < st["lane_efficiency"] <= 1.0
+    finally:
+        c.close()
+
+
 # ------------------------------------------------ graphs / async lists ----
 @pytest.mark.parametrize("fast", [False, True])
 @pytest.mark.parametrize("deck", ["dam3d", "random_overflow"])
