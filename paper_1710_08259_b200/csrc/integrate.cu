@@ -53,24 +53,38 @@ __global__ void k_symplectic(DomainDev d, long n, double* pos, double* v, const 
                              DevErr* err, const uint8_t* upd) {
     long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (k >= n || !active[k] || (upd && !upd[k])) return;  // ghosts: owned elsewhere
-    const double mk = mask ? mask[k] : 1.0;
+    // every load first (the compiler cannot move a load above a store through these
+    // pointers): ten independent requests in flight per thread instead of a chain
+    const double mk = mask ? __ldg(mask + k) : 1.0;
+    double xd[3] = {0.0, 0.0, 0.0}, vo[3] = {0.0, 0.0, 0.0}, xo[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        if (a < d.dim) {
+            xd[a] = __ldg(vdot + a * n + k);
+            vo[a] = v[a * n + k];
+            xo[a] = pos[a * n + k];
+        }
     double vn[3];
     bool bad = false;
-    for (int a = 0; a < d.dim; ++a) {
-        // euler(v, vdot*mask, dt): vdot*mask is mask * vdot (scalar broadcast, tensor.cpp:55-57)
-        double xd = mask ? mk * vdot[a * n + k] : vdot[a * n + k];
-        vn[a] = v[a * n + k] + dt * xd;
-        bad |= !isfinite(vn[a]);
-        v[a * n + k] = vn[a];
-    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        if (a < d.dim) {
+            // euler(v, vdot*mask, dt): vdot*mask is mask * vdot (scalar broadcast, tensor.cpp:55-57)
+            const double x1 = mask ? mk * xd[a] : xd[a];
+            vn[a] = vo[a] + dt * x1;
+            bad |= !isfinite(vn[a]);
+            v[a * n + k] = vn[a];
+        }
     if (bad) latch_error(err, 2, kMsgNan, orig[k]);
     bad = false;
     unsigned long long warn = 0;
-    for (int a = 0; a < d.dim; ++a) {
-        double x = pos[a * n + k] + dt * vn[a];
-        bad |= !isfinite(x);
-        pos[a * n + k] = x;
-    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        if (a < d.dim) {
+            const double x = xo[a] + dt * vn[a];
+            bad |= !isfinite(x);
+            pos[a * n + k] = x;
+        }
     if (bad) latch_error(err, 2, kMsgNan, orig[k]);
     // apply_boundary_shift (particle_system.cpp:56-90)
     for (int a = 0; a < d.dim; ++a) {
