@@ -74,11 +74,15 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # plumbing checks on a single-GPU box: every rank on one device over gloo
+        # (NAU_BENCH_DEVICE=0 NAU_DIST_BACKEND=gloo); never a measurement
+        if "NAU_BENCH_DEVICE" in os.environ:
+            self.local = int(os.environ["NAU_BENCH_DEVICE"])
         self.pg = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            backend = os.environ.get("NAU_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend)
