@@ -139,6 +139,14 @@ class Exchanger:
         if self.world == 1:
             return None, None
         dev = self.device
+        # gloo moves P2P messages from host memory only: device rows are staged through
+        # the host (multi-rank plumbing checks on a one-GPU box; NCCL sends device rows)
+        staged = str(dev) != "cpu" and d.get_backend() == "gloo"
+        out_dev = dev
+        if staged:
+            dev = "cpu"
+            to_left = None if to_left is None else to_left.cpu()
+            to_right = None if to_right is None else to_right.cpu()
         n_l = 0 if to_left is None else to_left.shape[0]
         n_r = 0 if to_right is None else to_right.shape[0]
         cnt_s = torch.tensor([n_l, n_r], dtype=torch.int64, device=dev)
@@ -168,6 +176,8 @@ class Exchanger:
         if ops:
             for w in d.batch_isend_irecv(ops):
                 w.wait()
+        if staged:
+            from_left, from_right = from_left.to(out_dev), from_right.to(out_dev)
         return (from_left if self.left is not None else None,
                 from_right if self.right is not None else None)
 
@@ -211,6 +221,15 @@ class SlabRank:
 
     # ---- one step ----
     def step(self):
+        """One step of the §8(e) schedule. The backend's device work and the row tensors of
+        the exchange must share one stream: the CUDA backend makes its context's stream
+        torch's current stream for the whole step (`on_stream`), so a pack kernel and the
+        NCCL send of its rows are ordered without host synchronisation."""
+        import contextlib
+        with getattr(self.b, "on_stream", contextlib.nullcontext)():
+            self._step()
+
+    def _step(self):
         b = self.b
         if b.halo_values and self.x.world > 1:
             b.passes("density")
@@ -343,6 +362,12 @@ class GpuBackend:
         self.col_flag = self.width - 1
         self.device = f"cuda:{torch.cuda.current_device()}"
         ctx._check(ctx.L.nau_set_ghost_field(ctx.h, self.flag_id))
+
+    def on_stream(self):
+        """torch's current stream := the context's stream (row tensors, NCCL and the
+        library's kernels then run in one order)."""
+        torch = self.torch
+        return torch.cuda.stream(torch.cuda.ExternalStream(self.ctx.L.nau_get_stream(self.ctx.h)))
 
     # ---- passes ----
     def passes(self, k):

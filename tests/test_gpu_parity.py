@@ -859,8 +859,9 @@ class _ThreadExchanger:
         return t
 
 
+@pytest.mark.parametrize("fast", [False, True])
 @pytest.mark.parametrize("world", [2, 3])
-def test_slab_ranks_with_rebalancing_match_plain(ctx, world):
+def test_slab_ranks_with_rebalancing_match_plain(ctx, world, fast):
     """SURVEY.md §8(e) on the CUDA backend: `world` slab ranks (threads, one context each,
     one GPU) from skewed bounds with migration, ghost refresh and re-balancing every 3
     steps; owned particles gathered by global id = the single-context path, bitwise."""
@@ -877,11 +878,12 @@ def test_slab_ranks_with_rebalancing_match_plain(ctx, world):
     steps = 9
     plain = bench.DamBreak(2)
     plain.sc = scene()
-    ctx.set_mode(False)
+    ctx.set_mode(fast)  # FAST: the paired-list kernels with ghosts in the lists
     plain.setup(ctx)
     for _ in range(steps):
         plain.step(ctx)
     ref_r, ref_v = ctx.download("r"), ctx.download("v")
+    ctx.set_mode(False)
     hub = _Hub(world)
     out, errs, drv = {}, [], {}
 
@@ -891,6 +893,7 @@ def test_slab_ranks_with_rebalancing_match_plain(ctx, world):
                 pg = None
             D.world, D.rank, D.local = world, rank, 0
             c = nau.Context(0)
+            c.set_mode(fast)
             sl = bench.DamBreakSlab(2, D())
             sl.sc = scene()
             sl.setup(c)
