@@ -23,3 +23,15 @@ def test_slab_ranks_as_processes_match_plain(world, mode):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "two_process_slab OK" in r.stdout
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_nbody_shards_as_processes_match_plain(world, mode):
+    port = 29700 + 10 * world + (mode == "fast")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "tests", "two_process_slab.py"), mode, "nbody"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "two_process_slab OK" in r.stdout

@@ -24,11 +24,46 @@ def scene():
     return sc
 
 
+def nbody(d, fast):
+    """cfg4's sharded path: broadcast-pipelined source chunks (slab.pipelined_sources +
+    nau_gravity_sources_part) against the plain leapfrog, bitwise."""
+    n = 1536  # divisible by 2 and 3
+    ctx = nau.Context(0)
+    ctx.set_mode(fast)
+    sh = bench.GravityShard(d)
+    sh.sc = scenes.plummer(n=n)
+    sh.setup(ctx)
+    for _ in range(3):
+        sh.step(ctx)
+    ctx.sync()
+    mine = np.concatenate([ctx.download("r"), ctx.download("v"), ctx.download("a")]).T.copy()
+    parts = [None] * d.world
+    dist.gather_object(mine, parts if d.rank == 0 else None, dst=0)
+    ok = True
+    if d.rank == 0:
+        plain = bench.Gravity()
+        plain.sc = scenes.plummer(n=n)
+        c1 = nau.Context(0)
+        c1.set_mode(fast)
+        plain.setup(c1)
+        for _ in range(3):
+            plain.step(c1)
+        ref = np.concatenate([c1.download("r"), c1.download("v"), c1.download("a")]).T
+        ok = np.array_equal(np.concatenate(parts), ref)
+        print("two_process_slab", "OK" if ok else "MISMATCH", d.world, "ranks nbody",
+              "fast" if fast else "exact", flush=True)
+    return ok
+
+
 def main():
     fast = sys.argv[1] == "fast"
     os.environ["NAU_BENCH_DEVICE"] = "0"
     os.environ["NAU_DIST_BACKEND"] = "gloo"
     d = bench.Dist()
+    if len(sys.argv) > 2 and sys.argv[2] == "nbody":
+        ok = nbody(d, fast)
+        d.close()
+        sys.exit(0 if ok else 1)
     ctx = nau.Context(0)
     ctx.set_mode(fast)
     sl = bench.DamBreakSlab(2, d)
