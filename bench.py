@@ -835,6 +835,9 @@ def run_ours(args, dist):
     wl = make_workload(args.config, dist, use_slab, args.comm == "native")
     ctx = nau.Context(dist.local)
     ctx.set_mode(args.mode == "fast")
+    # one stream for everything: torch's row tensors, copies and collectives run in the
+    # context's stream order (warm-up steps included), never beside the library's kernels
+    torch.cuda.set_stream(torch.cuda.ExternalStream(ctx.L.nau_get_stream(ctx.h)))
     wl.setup(ctx)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=f"cuda:{dist.local}")
     for _ in range(args.warmup):
