@@ -849,12 +849,15 @@ __device__ __forceinline__ void build_pair_list(const Geo& g, const float4* __re
                                                 bool has1, Emit&& emit, Mark&& mark) {
     const int k1 = k0 + 1;
     if (hg.on && *hg.escaped == 0) {
-        if (has1 && g.key[k0] == g.key[k1]) {
-            const int ks[2] = {k0, k1};
-            half_scan<DIM, false, 2, true>(g, hg, ks,
-                                           [&](uint32_t v, const uint32_t* m) { emit(v, m[0]); });
-        } else {
-            build_list_half<DIM, false>(g, hg, k0, emit);
+        // one pass of the same code for every lane: a particle without a partner in its
+        // cell is scanned as the pair (k0, k0), so a warp with a straddling pair pays that
+        // pair's second scan only (once a flow has dissolved the lattice about every
+        // second warp holds one)
+        const bool shared = has1 && g.key[k0] == g.key[k1];
+        const int ks[2] = {k0, shared ? k1 : k0};
+        half_scan<DIM, false, 2, true>(g, hg, ks,
+                                       [&](uint32_t v, const uint32_t* m) { emit(v, m[0]); });
+        if (!shared) {
             mark();
             if (has1) build_list_half<DIM, false>(g, hg, k1, emit);
         }

@@ -67,6 +67,14 @@ def main():
                "lane_eff": round(st["lane_efficiency"], 3)}
         print(json.dumps(row), flush=True)
         assert np.isfinite(v).all() and np.isfinite(rho).all()
+    # per-kernel times in the evolved state (launch events; plain steps)
+    c.profile(True)
+    for _ in range(5):
+        c.wcsph_step(p)
+    c.sync()
+    names = {300: "cell build", 302: "list build", 200: "density", 201: "momentum", 301: "symplectic"}
+    print(json.dumps({"evolved_ms": {v: round(c.profile_ms(k)[0] / max(c.profile_ms(k)[1], 1), 4)
+                                     for k, v in names.items()}}), flush=True)
     c.close()
 
 
