@@ -1039,7 +1039,7 @@ def _scene(config):
             0: lambda: scenes.dam_break(2), 3: scenes.dem_column, 4: scenes.plummer}[config]()
 
 
-def cpu_baseline(args, wl=None, full_steps=None):
+def cpu_baseline(args, wl=None, full_steps=None, sample_steps=None):
     """Time the reference's own CPU path (oracle/_ref) on the box's host cores:
     (1) `full_steps` full-N Case::solve_step(ThreadPool(P)) calls (SURVEY.md §8(d)'s
     anchor; skipped when None), and (2) the bounded sample estimate: build_cells over
@@ -1106,6 +1106,32 @@ def cpu_baseline(args, wl=None, full_steps=None):
         out["value"] = round(est, 1)
         out["sample"] = (f"reference Case path (oracle/_ref, unmodified sources): {sample}; "
                          f"{kernel_note}; host CPU: {model}")
+    if sample_steps:
+        # the reference arm's K timed steps: each a bounded sample of the step (a full
+        # build_cells + every equation's RHS over the same spread particles), sized so that
+        # warm-up + K steps take ~2 minutes; the full-N anchor above stays the value
+        k_steps, w_steps = sample_steps
+        budget = 120.0 / max(1, k_steps + w_steps)
+        per_rhs = t / cnt
+        ns = int(min(n, max(64 * threads, (budget - t_build) / max(per_rhs, 1e-12))))
+
+        def one():
+            s0 = time.perf_counter()
+            rc.build_cells()
+            _, m = sample_cost(ns)
+            return time.perf_counter() - s0, m
+
+        for _ in range(w_steps):
+            one()
+        ts, m = [], ns
+        for _ in range(k_steps):
+            dt_s, m = one()
+            ts.append(dt_s)
+        mean = sum(ts) / max(len(ts), 1)
+        out["sample_steps"] = {"steps": k_steps, "warmup": w_steps, "particles_per_step": m,
+                               "mean_s": round(mean, 4), "min_s": round(min(ts), 4),
+                               "max_s": round(max(ts), 4),
+                               "full_step_estimate": round(1.0 / (t_build / n + (mean - t_build) / m), 1)}
     del rc
     return out
 
@@ -1119,21 +1145,30 @@ REF_FULL_STEPS = {0: 20, 1: 1, 2: 1, 3: 2, 4: 1}
 
 
 def run_reference(args, dist):
+    """The reference arm: the unmodified reference (oracle/_ref) on the box's host threads.
+    `value` = N x steps / time of full-N Case::solve_step calls (the anchor SURVEY.md §8(d)
+    asks for); the --steps K / --warmup W steps the contract counts are bounded SAMPLES of
+    that step (a full build_cells + every equation's RHS over a fixed spread of particles),
+    so ms_per_step x K is the wall time actually spent in them."""
     if dist.rank != 0:
         return None
-    cb = cpu_baseline(args, full_steps=REF_FULL_STEPS[args.config])
-    per_step_ms = None
+    cb = cpu_baseline(args, full_steps=REF_FULL_STEPS[args.config],
+                      sample_steps=(args.steps, args.warmup))
     n = _scene(args.config).n if cb["value"] else None
-    if cb["value"]:
-        per_step_ms = n / cb["value"] * 1e3
+    ss = cb.get("sample_steps")
+    per_step_ms = ss["mean_s"] * 1e3 if ss else (n / cb["value"] * 1e3 if cb["value"] else None)
     return {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "particle-updates/s",
             "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms,
+            "ms_per_full_step": (n / cb["value"] * 1e3) if cb["value"] else None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": WORKLOAD_NAMES[args.config], "threads": cb["cores"],
-                       "timed": (f"{cb.get('full_steps', {}).get('steps')} full-N "
+                       "timed": (f"value: {cb.get('full_steps', {}).get('steps')} full-N "
                                  "Case::solve_step call(s) on all host threads (the reference's "
-                                 "whole step; --steps/--warmup do not apply)")},
+                                 "whole step); steps/warmup/ms_per_step: bounded sample steps ("
+                                 f"{ss['particles_per_step'] if ss else 0} particles' RHS + a full "
+                                 "build_cells each), whose full-step estimate is "
+                                 f"{ss['full_step_estimate'] if ss else None} particle-updates/s")},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "particle-updates/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
