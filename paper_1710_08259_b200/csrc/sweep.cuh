@@ -675,10 +675,34 @@ __device__ __forceinline__ void half_scan(const Geo& g, const HalfGrid& hg, cons
         uint32_t icode;
         int s, ns, ps;
     };
+    // option digits without integer divisions: an odometer counting up from the first
+    // option and (balanced order) one counting down from the last, used alternately —
+    // setup(idx) is called for idx = 0, 1, 2, ... exactly once each
+    int up[3] = {0, 0, 0};
+    int dn[3] = {ao[0].cnt - 1, DIM > 1 ? ao[1].cnt - 1 : 0, DIM > 2 ? ao[2].cnt - 1 : 0};
     auto setup = [&](int idx, Opt& o) {
-        const int combo = ORDERED ? idx : ((idx & 1) ? ncombo - 1 - (idx >> 1) : (idx >> 1));
-        const int oo[3] = {combo % ao[0].cnt, DIM > 1 ? (combo / ao[0].cnt) % ao[1].cnt : 0,
-                           DIM > 2 ? combo / n01 : 0};
+        int oo[3];
+        if (ORDERED || !(idx & 1)) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) oo[a] = up[a];
+            if (++up[0] == ao[0].cnt) {
+                up[0] = 0;
+                if (DIM > 1 && ++up[1] == ao[1].cnt) {
+                    up[1] = 0;
+                    ++up[2];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) oo[a] = dn[a];
+            if (--dn[0] < 0) {
+                dn[0] = ao[0].cnt - 1;
+                if (DIM > 1 && --dn[1] < 0) {
+                    dn[1] = ao[1].cnt - 1;
+                    --dn[2];
+                }
+            }
+        }
         int flat = 0, code = 0, stride = 1, scode = 1;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
