@@ -60,7 +60,7 @@ constexpr int kHashIlp = 4;
 
 template <bool AGG>
 __global__ void k_hash(DomainDev d, long n, const double* pos, const uint8_t* active,
-                       const int* orig, int* key, int* count, DevErr* err) {
+                       const int* orig, int* key, int* count, int* arrival, DevErr* err) {
     const long base = (long)blockIdx.x * blockDim.x * kHashIlp + threadIdx.x;
     double x[kHashIlp][3];
     bool act[kHashIlp];
@@ -88,17 +88,23 @@ __global__ void k_hash(DomainDev d, long n, const double* pos, const uint8_t* ac
                 flat = flat * d.cells[a] + cell_index(d, a, xa);
             }
         }
+        // arrival[k] = this particle's place among its cell's arrivals (the counter's old
+        // value): the scatter needs no second round of atomics
         if (!AGG) {
             if (valid) {
                 key[k] = flat;
-                atomicAdd(&count[flat], 1);
+                arrival[k] = atomicAdd(&count[flat], 1);
             }
             continue;
         }
         const unsigned peers = __match_any_sync(0xffffffffu, valid ? flat : -1);
+        const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+        int base = 0;
+        if (valid && lane == leader) base = atomicAdd(&count[flat], __popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
         if (!valid) continue;
         key[k] = flat;
-        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[flat], __popc(peers));
+        arrival[k] = base + __popc(peers & ((1u << lane) - 1u));
     }
 }
 
@@ -174,28 +180,13 @@ __global__ void k_scan_add(int* out, long n, const int* tile_sums) {
         if (base + i < n) out[base + i] += add;
 }
 
-// AGG: warp-aggregated cursor, the lanes of one cell take consecutive slots after
-// one atomic (the within-cell order is fixed by k_rank afterwards).
-template <bool AGG>
-__global__ void k_scatter(long n, const int* key, const int* orig, const int* start, int* cursor,
-                          int* perm_tmp, int* okey) {
+// Slot = the cell's start + the arrival place k_hash took (the within-cell order is
+// fixed by k_rank afterwards).
+__global__ void k_scatter(long n, const int* key, const int* orig, const int* start,
+                          const int* arrival, int* perm_tmp, int* okey) {
     const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    const bool valid = k < n;
-    const int c = valid ? key[k] : -1;
-    if (!AGG) {
-        if (!valid) return;
-        const int slot = start[c] + atomicAdd(&cursor[c], 1);
-        perm_tmp[slot] = (int)k;
-        okey[slot] = orig[k];
-        return;
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, c);
-    const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
-    int base = 0;
-    if (valid && lane == leader) base = atomicAdd(&cursor[c], __popc(peers));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (!valid) return;
-    const int slot = start[c] + base + __popc(peers & ((1u << lane) - 1u));
+    if (k >= n) return;
+    const int slot = start[key[k]] + arrival[k];
     perm_tmp[slot] = (int)k;
     okey[slot] = orig[k];
 }
@@ -501,28 +492,24 @@ void launch_build_cells(nau_ctx* c) {
     const long n = c->n;
     const int nc = c->dom.ncells;
     cudaMemsetAsync(c->d_cell_count, 0, sizeof(int) * (nc + 1), c->stream);
-    cudaMemsetAsync(c->d_cursor, 0, sizeof(int) * (nc + 1), c->stream);
     const bool agg = n >= 8L * nc;  // >= 8 particles per cell on average
     if (n > 0) {
+        // d_perm doubles as the arrival places until k_rank writes the permutation
         if (agg)
             k_hash<true><<<blocks_for(n, kBlock * kHashIlp), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_active,
                                                                   c->d_orig, c->d_key, c->d_cell_count,
-                                                                  c->d_err);
+                                                                  c->d_perm, c->d_err);
         else
             k_hash<false><<<blocks_for(n, kBlock * kHashIlp), kBlock, 0, c->stream>>>(c->dom, n, c->fields[0].d, c->d_active,
                                                                    c->d_orig, c->d_key, c->d_cell_count,
-                                                                   c->d_err);
+                                                                   c->d_perm, c->d_err);
         c->launches++;
     }
     // cell_start[ncells] (start of the inactive tail bin) = number of active particles.
     scan_exclusive(c, c->d_cell_count, c->d_cell_start, nc + 1);
     if (n == 0) return;
-    if (agg)
-        k_scatter<true><<<blocks_for(n), kBlock, 0, c->stream>>>(n, c->d_key, c->d_skey, c->d_cell_start,
-                                                                 c->d_cursor, c->d_perm_tmp, c->d_okey);
-    else
-        k_scatter<false><<<blocks_for(n), kBlock, 0, c->stream>>>(n, c->d_key, c->d_skey, c->d_cell_start,
-                                                                  c->d_cursor, c->d_perm_tmp, c->d_okey);
+    k_scatter<<<blocks_for(n), kBlock, 0, c->stream>>>(n, c->d_key, c->d_skey, c->d_cell_start,
+                                                       c->d_perm, c->d_perm_tmp, c->d_okey);
     // (okey = the within-cell sort key: original index, or a slab's global id)
     k_rank<<<blocks_for(n), kBlock, 0, c->stream>>>(n, nc, c->d_key, c->d_cell_start,
                                                     c->d_cell_count, c->d_perm_tmp, c->d_okey,
