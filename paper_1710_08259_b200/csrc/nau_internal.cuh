@@ -129,9 +129,22 @@ struct FieldBuf {
 // 32-byte gather in ONE load instruction (sm_100: LDG.E.ENL2.256). The pair
 // gathers of the neighbour sums are bound by L1 wavefronts; a double4 read as
 // two 128-bit loads costs two (profiles/r1_nl_*: L1/TEX throughput ~85%).
+#ifndef NAU_LD256
+#define NAU_LD256 1  // non-coherent path: every ld256 source is read-only in the kernel that gathers it
+#endif
 __device__ __forceinline__ double4 ld256(const double4* p) {
     double4 v;
+#if NAU_LD256 == 1
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+#elif NAU_LD256 == 2
+    asm("ld.global.L1::evict_last.v4.f64 {%0, %1, %2, %3}, [%4];"
+#elif NAU_LD256 == 3
+    asm("ld.global.nc.L1::evict_last.v4.f64 {%0, %1, %2, %3}, [%4];"
+#elif NAU_LD256 == 4
+    asm("ld.global.L2::256B.v4.f64 {%0, %1, %2, %3}, [%4];"
+#else
     asm("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+#endif
         : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
         : "l"(p));
     return v;
