@@ -4,6 +4,7 @@ re-balancing equals a single-context run bitwise. The thread-rank test of
 test_gpu_parity.py covers the rank logic; this one covers the process path — torch row
 tensors, the exchange and the library's kernels ordered on one stream."""
 import os
+import socket
 import subprocess
 import sys
 
@@ -13,10 +14,18 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 @pytest.mark.parametrize("mode", ["exact", "fast"])
 @pytest.mark.parametrize("world", [2, 3])
 def test_slab_ranks_as_processes_match_plain(world, mode):
-    port = 29600 + 10 * world + (mode == "fast")
+    port = free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "two_process_slab.py"), mode]
@@ -28,7 +37,7 @@ def test_slab_ranks_as_processes_match_plain(world, mode):
 @pytest.mark.parametrize("mode", ["exact", "fast"])
 @pytest.mark.parametrize("world", [2, 3])
 def test_nbody_shards_as_processes_match_plain(world, mode):
-    port = 29700 + 10 * world + (mode == "fast")
+    port = free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "two_process_slab.py"), mode, "nbody"]
